@@ -1,0 +1,359 @@
+"""Benchmark of the PP-GNN mini-batch loading hot path (arXiv 2504.13266) on B200.
+
+A "step" is one epoch of the whole hot path: pp_epoch_permute
+(SGD-RR Philox argsort) + every batch of the epoch assembled with the fused
+fp32 -> bf16 cast (one pp_next_batch call per batch).  value = nodes/s.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--chunk c]
+                  [--per-call k]  (k batches per pp_next_batches launch; 1 = pp_next_batch)
+
+N = 1: ogbn-products-shaped (BASELINE configs[1]): N = 2,449,029, F = 100, K = 3 (H = 4),
+B = 8192, HBM-resident fp32 hop features (synthetic, §8(d) generator G), bf16 batches.
+N > 1 (torchrun): ogbn-papers100M-shaped (configs[2]): N = 111,059,956, F = 128, K = 3,
+B = 8192 per rank, chunk reshuffle c = 8192, nodes sharded round-robin over the ranks,
+rows read from the owners' HBM by NVLink peer loads (CUDA IPC).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batch-assembly nodes/sec"
+UNIT = "nodes/s"
+SEED0 = 250413266
+DATA_SEED = 2504
+
+CONFIGS = {
+    "products": dict(N=2_449_029, H=4, F=100, B=8192, chunk=1),
+    "papers100M": dict(N=111_059_956, H=4, F=128, B=8192, chunk=8192),
+    "tiny": dict(N=2708, H=4, F=128, B=256, chunk=1),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def committed_traffic(name: str):
+    """dram read+write bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(name)
+    return None
+
+
+# --------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
+def oracle_epoch_sample(cfg, nbatches: int, nthreads: int):
+    """The oracle as it stands: permutation of all N units (qsort, 1 thread) + gather+cast of
+    the first `nbatches` batches from a host store regenerated with the oracle generator (all rows,
+    untimed).  Returns (extrapolated epoch seconds, timings)."""
+    import numpy as np
+
+    import oracle
+
+    N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
+    store = oracle.gen_rows(DATA_SEED, oracle.F32, H, F, np.arange(N), nthreads=nthreads)  # [N, H, F] node-major
+    t0 = time.perf_counter()
+    order = oracle.epoch_order(SEED0, N, chunk)
+    t1 = time.perf_counter()
+    steps = oracle.num_steps(N, B)
+    nb = min(nbatches, steps)
+    rows_done = 0
+    for t in range(nb):
+        s, e = oracle.batch_range(N, B, 1, t, 0)
+        oracle.gather_cast(store, oracle.F32, F, H * F, H, F, order[s:e], oracle.BF16, nthreads=nthreads)
+        rows_done += e - s
+    t2 = time.perf_counter()
+    epoch_s = (t1 - t0) + (t2 - t1) * (N / rows_done)
+    return epoch_s, {"permute_s": t1 - t0, "gather_s": t2 - t1, "gather_rows": rows_done, "batches": nb}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier has no runnable reference code)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS["products"]
+    nthreads = os.cpu_count() or 1
+    times = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        s, info = oracle_epoch_sample(cfg, 16, nthreads)
+        if i >= args.warmup:
+            times.append(s)
+    ms = statistics.median(times) * 1e3
+    value = cfg["N"] / (ms / 1e3)
+    sample = (f"per step: full-N permutation + gather+cast of {info['batches']} of 299 batches "
+              f"({info['gather_rows']} rows), epoch time extrapolated by rows")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32->bf16", "data": "synthetic",
+        "config": config_dict("products", cfg, 1, "none (host)"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def config_dict(name, cfg, W, l2):
+    return {"workload": f"{name}-shaped", "num_nodes": cfg["N"], "feat_dim": cfg["F"], "hops_K": cfg["H"] - 1,
+            "batch_size": cfg["B"], "chunk": cfg["chunk"], "store": "fp32 node-major, HBM-resident",
+            "out": "bf16", "world_size": W, "l2_policy": l2}
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+
+    import paper_2504_13266_b200 as pp
+
+    W = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if W > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = args.config or ("products" if W == 1 else "papers100M")
+    cfg = dict(CONFIGS[name])
+    if args.chunk is not None:
+        cfg["chunk"] = args.chunk
+    N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
+    stream = torch.cuda.Stream()
+
+    desc = dict(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
+                device=local)
+    if W > 1:
+        desc.update(world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
+    L = pp.Loader(**desc)
+    L.fill_synthetic(DATA_SEED)
+    if W > 1:
+        h = pp.pp_export_store(L.h)
+        hs = [None] * W
+        dist.all_gather_object(hs, h)
+        pp.pp_import_peer_stores(L.h, b"".join(hs))
+    L.set_stream(stream)
+    info = L.query()
+    steps = info["steps_per_epoch"]
+    rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
+
+    # output ring: one slot per step of the epoch (> L2: outputs really go to DRAM)
+    ring = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
+    slot_bytes = B * H * F * 2
+    k = max(1, args.per_call)
+
+    def epoch(e, ev_mid=None):
+        L.epoch_permute(SEED0 + e, chunk, stream)
+        if ev_mid is not None:
+            ev_mid.record(stream)
+        done = 0
+        while done < steps:
+            if k == 1:
+                L.next_batch(ring[done], None, None, stream)
+                done += 1
+            else:
+                done += len(L.next_batches(min(k, steps - done), ring[done], slot_bytes, None, None, stream))
+
+    # rows this rank assembles per epoch (for the algorithmic bytes)
+    my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
+    launches_per_epoch = (6 + (2 if chunk > 1 else 0)) + (steps if k == 1 else -(-steps // k))
+
+    with torch.cuda.stream(stream):
+        for e in range(args.warmup):
+            epoch(e)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for i in range(args.steps):
+                evs[i][0].record(stream)
+                epoch(args.warmup + i, evs[i][1])
+                evs[i][2].record(stream)
+            end.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = start.elapsed_time(end)
+    gather_ms = sum(b.elapsed_time(c) for _, b, c in evs)
+    perm_ms = sum(a.elapsed_time(b) for a, b, _ in evs)
+    if dist:
+        t = torch.tensor([total_ms, gather_ms, perm_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, gather_ms, perm_ms = t.tolist()
+    ms_per_step = total_ms / args.steps
+    value = N * args.steps / (total_ms / 1e3)  # all ranks together assemble N rows per epoch
+
+    peak, peak_kind = peaks()
+    gather_launches = steps if k == 1 else -(-steps // k)
+    per_launch_ms = gather_ms / (args.steps * gather_launches)
+    bytes_per_launch = my_rows * (rec_in + rec_out + 4) / gather_launches
+    achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": committed_traffic(f"gather_{name}_k{k}"), "kernel": "k_gather_vec<bf16>",
+                "peak_kind": peak_kind, "per_launch_us": per_launch_ms * 1e3,
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "frac_of_8TBs_nominal": achieved / 8000.0,
+                "permute_ms_per_epoch": perm_ms / args.steps}
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if W == 1 else "strong",
+        "vs_baseline": None, "dtype": "f32->bf16", "data": "synthetic (§8(d) generator G, filled in place)",
+        "config": config_dict(name, cfg, W, "inputs > L2 (3.9 GB store), outputs rotate over a "
+                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring"),
+        "roofline": roofline, "gpu_launches": launches_per_epoch * args.steps, "clocks": clk.summary(),
+        "batches_per_launch": k,
+    }
+    del ring
+    L.close()
+    torch.cuda.empty_cache()
+
+    if W == 1 and not args.skip_e2e:
+        result["e2e"] = e2e_host_store(pp, torch, cfg, args)
+    if rank == 0 and W == 1 and not args.skip_cpu:
+        nthreads = os.cpu_count() or 1
+        s, inf = oracle_epoch_sample(cfg, 32, nthreads)
+        result["cpu_baseline"] = {
+            "value": N / s, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": (f"full-N permutation (1 thread, qsort) + gather+cast of {inf['batches']} batches "
+                       f"({inf['gather_rows']} rows, {nthreads} OpenMP threads); epoch extrapolated by rows"),
+            "permute_s": inf["permute_s"], "gather_s": inf["gather_s"]}
+    if rank == 0:
+        print(json.dumps(result))
+    if dist:
+        dist.destroy_process_group()
+
+
+def e2e_host_store(pp, torch, cfg, args):
+    """Same epoch with the hop store in pinned host memory (the paper's host placement,
+    PAPER.md:287-288): every feature byte crosses host->device inside the timed region
+    (UVA zero-copy reads), and each batch's node ids are read back to host."""
+    N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
+    L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
+                  hbm_budget_bytes=-1)
+    L.fill_synthetic(DATA_SEED)
+    stream = torch.cuda.Stream()
+    L.set_stream(stream)
+    info = L.query()
+    steps = info["steps_per_epoch"]
+    out = [torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    nodes = torch.empty((steps, B), dtype=torch.int64, device="cuda")
+    host_nodes = torch.empty((steps, B), dtype=torch.int64, pin_memory=True)
+
+    def epoch(e):
+        L.epoch_permute(SEED0 + e, chunk, stream)
+        for t in range(steps):
+            L.next_batch(out[t % 2], None, nodes[t], stream)
+        host_nodes.copy_(nodes, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        epoch(0)
+    torch.cuda.synchronize()
+    reps = 2
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for i in range(reps):
+            epoch(1 + i)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    L.close()
+    return {"value": N / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": N * info["record_bytes_in"],
+            "d2h_bytes_per_step": N * 8, "ms_per_step": ms,
+            "how": "store in pinned host memory, read zero-copy over PCIe by the gather kernel; node ids D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--per-call", type=int, default=1, help="batches per launch (pp_next_batches)")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        import __graft_entry__ as ge
+
+        ge.build()
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

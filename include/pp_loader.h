@@ -1,0 +1,230 @@
+/*
+ * pp_loader.h -- C ABI of libppload.so, a B200-native (sm_100a) mini-batch
+ * loader for pre-propagation GNNs (PP-GNNs), the hot path that arXiv
+ * 2504.13266 ("Graph Learning at Scale: Characterizing and Optimizing
+ * Pre-Propagation GNNs") optimises.
+ *
+ * What the library computes (PAPER.md line numbers are lines of the paper's
+ * LaTeX source; "Ox" are the oracle steps of SURVEY.md §8(c)):
+ *   - Input: the K+1 pre-propagated hop matrices X_k = B^k X, k = 0..K, with
+ *     B = D~^{-1/2}(I+A)D~^{-1/2} (Eq. (2)), each
+ *     [N_total, F], plus an optional training-node set and labels.
+ *   - pp_epoch_permute: the per-epoch shuffle.  chunk = 1 is SGD-RR, a fresh
+ *     uniform row permutation; chunk = c > 1 is the paper's
+ *     chunk reshuffling, "reshuffle training data indices at the chunk level,
+ *     with each chunk comprising contiguous node features".
+ *     The permutation is the argsort of 64-bit Philox4x32-10 keys (O4-O7).
+ *   - pp_next_batch: batch assembly, "copy the scattered node features into"
+ *     one contiguous batch, done on the GPU: out[j,k,f] =
+ *     cast(X_k[v_j, f]) with the fp32 -> bf16/fp16 round-to-nearest-even cast
+ *     fused in (O9, O10).  Asynchronous on a loader stream with an event
+ *     handoff to the consumer stream: the paper's double-buffer prefetch on
+ *     separate streams when the caller alternates two
+ *     output buffers.
+ *   - Rows beyond the HBM budget live in pinned, mapped host memory and are
+ *     read zero-copy over PCIe (host placement).
+ *   - W > 1: nodes are sharded round-robin over W GPUs (owner(v) = v mod W,
+ *     local row v div W; "distributing data across multiple GPUs",
+ *     PAPER.md:285) and each rank reads the rows of its batch from the
+ *     owners' HBM by peer (NVLink) loads.
+ *
+ * Conventions for every entry point:
+ *   - Every call returns pp_status; no C++ exception crosses the ABI.
+ *   - PP_ERR_INVALID: bad arguments, no side effects.  pp_last_error() has a
+ *     message (thread-local, valid until the next failing call on the thread).
+ *   - PP_ERR_CUDA / PP_ERR_NCCL are sticky: the handle is poisoned and only
+ *     pp_loader_destroy is valid afterwards.
+ *   - One handle is used by one host thread at a time.
+ *   - "stream" arguments are cudaStream_t values passed as void*; NULL is the
+ *     legacy default stream.
+ */
+#ifndef PP_LOADER_H
+#define PP_LOADER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_ABI_VERSION 1
+
+typedef struct pp_loader pp_loader; /* opaque handle */
+
+typedef enum {
+  PP_OK = 0,
+  PP_ERR_INVALID = 1,   /* bad argument; no side effects */
+  PP_ERR_OOM = 2,       /* device or pinned-host allocation failed */
+  PP_ERR_CUDA = 3,      /* CUDA runtime error; handle poisoned */
+  PP_ERR_NCCL = 4,      /* reserved for a collective transport; handle poisoned */
+  PP_ERR_STATE = 5,     /* call out of order (e.g. next_batch before any permute) */
+  PP_END_OF_EPOCH = 6   /* cursor exhausted; *rows = 0, nothing enqueued */
+} pp_status;
+
+typedef enum { PP_F32 = 0, PP_BF16 = 1, PP_F16 = 2 } pp_dtype;
+typedef enum { PP_MEM_HOST = 0, PP_MEM_DEVICE = 1 } pp_mem;
+
+/* How the W ranks of a sharded loader reach each other's stores. */
+typedef enum {
+  PP_PEERS_NONE = 0,     /* W == 1 */
+  PP_PEERS_IPC = 1,      /* one process per GPU; handles exchanged with
+                            pp_export_store / pp_import_peer_stores */
+  PP_PEERS_LOOPBACK = 2  /* W shards in ONE process on ONE device, linked with
+                            pp_link_loopback (tests the sharded path on 1 GPU) */
+} pp_peers;
+
+/* The K+1 hop matrices X_0..X_K.
+ *   elem(k, v, f) = data[k*hop_stride + v*row_stride + f]   (element units)
+ *   hop-major [H][N][F]: hop_stride = N*F, row_stride = F
+ *   node-major [N][H][F]: hop_stride = F,   row_stride = H*F
+ * Requirements: row_stride >= F.  data == NULL: allocate the store only
+ * (fill it with pp_fill_synthetic).  For W > 1, data (if given) covers all
+ * N rows; rank r copies only the rows it owns (v mod W == r). */
+typedef struct {
+  const void* data;
+  pp_mem where;        /* memory space of data */
+  int64_t num_nodes;   /* N_total rows per hop matrix (>= 1, < 2^32) */
+  int32_t num_hops;    /* H = K + 1 (>= 1) */
+  int32_t feat_dim;    /* F (>= 1) */
+  int64_t hop_stride;  /* elements */
+  int64_t row_stride;  /* elements */
+  pp_dtype dtype;      /* PP_F32, PP_F16 or PP_BF16 */
+} pp_hop_desc;
+
+typedef struct {
+  pp_hop_desc hops;
+  const int64_t* node_set;  /* host, num_set ids in [0, N_total) (training nodes,
+                               PAPER.md:365); NULL => all rows 0..N_total-1 */
+  int64_t num_set;          /* ignored when node_set == NULL */
+  const int32_t* labels;    /* host, length N_total; NULL => no labels */
+  int32_t batch_size;       /* B rows per rank per step (>= 1) */
+  pp_dtype out_dtype;       /* PP_BF16 / PP_F16 (RNE cast from PP_F32), or
+                               == hops.dtype (bit copy) */
+  int32_t drop_last;        /* 0: keep the ragged last step; 1: drop it */
+  int64_t hbm_budget_bytes; /* bytes of HBM for this rank's store; rows
+                               beyond it spill to pinned mapped host memory.
+                               0 => (free HBM - 2 GiB reserve); < 0 => all
+                               rows in host memory (the paper's host
+                               placement).  W > 1 requires no spill. */
+  int32_t world_size;       /* W >= 1 */
+  int32_t rank;             /* 0 <= r < W */
+  pp_peers peers;           /* PP_PEERS_NONE iff W == 1 */
+  int32_t device;           /* CUDA device ordinal */
+} pp_loader_desc;
+
+/* Read-only facts about a loader (pp_loader_query). */
+typedef struct {
+  int64_t num_positions;    /* N: |node_set| or N_total */
+  int64_t num_nodes_total;  /* N_total */
+  int64_t local_rows;       /* rows owned by this rank */
+  int64_t rows_hbm;         /* of which in HBM */
+  int64_t rows_spill;       /* of which in pinned host memory (UVA) */
+  int64_t record_bytes_in;  /* H*F*s_in: bytes of one node record in the store */
+  int64_t record_stride;    /* store pitch between records (>= record_bytes_in, 16-B multiple) */
+  int64_t record_bytes_out; /* H*F*s_out: bytes of one output row */
+  int64_t steps_per_epoch;  /* ceil(N / (W*B)), or floor with drop_last */
+  int64_t cursor;           /* next step index */
+  int32_t permuted;         /* 1 after the first pp_epoch_permute */
+  int32_t gather_path;      /* 0 = vector (16-B) path, 1 = scalar fallback */
+} pp_loader_info;
+
+/* Create a loader.  Copies the hop data into a library-owned, node-major store
+ * [local_rows, H, F] (HBM part + optional pinned-host spill), uploads
+ * node_set / labels, and creates the loader stream.  Synchronous.
+ * Errors: PP_ERR_INVALID (null/out-of-range fields, node_set id out of range,
+ * unsupported dtype pair, W > 1 with spill), PP_ERR_OOM, PP_ERR_CUDA. */
+pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out);
+
+/* Release everything the handle owns (store, spill, order, streams, peer
+ * mappings).  Waits for the handle's outstanding work.  NULL is a no-op. */
+pp_status pp_loader_destroy(pp_loader* L);
+
+/* Start an epoch: compute order[] on the device from (seed, chunk) and reset
+ * the cursor to step 0.  1 <= chunk <= N (chunk = 1: SGD-RR; chunk = c:
+ * chunk reshuffling).  Runs on the loader stream after all work
+ * enqueued on `stream` so far; later pp_next_batch calls are ordered after it.
+ * Collective for W > 1: every rank passes the same (seed, chunk).
+ * Errors: PP_ERR_INVALID (chunk out of range), PP_ERR_CUDA. */
+pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream);
+
+/* Assemble this rank's batch of the current step into `out` and advance the
+ * cursor.  out: device, [B][H][F] of out_dtype, contiguous, caller-owned,
+ * 16-byte aligned for the vector path.  out_labels: device int32 [B] or NULL
+ * (must be NULL if the loader has no labels).  out_nodes: device int64 [B] or
+ * NULL (global node ids).  *rows receives the rows written (< B only in the
+ * last step; may be 0 on high ranks of the last step for W > 1).
+ * Stream semantics: `out` is written after all work enqueued on
+ * consumer_stream before this call, and is valid for work enqueued on
+ * consumer_stream after it.  Alternating two buffers therefore overlaps the
+ * assembly of batch t+1 with the consumer's work on batch t (double buffer).
+ * Errors: PP_ERR_STATE (no permute yet), PP_END_OF_EPOCH (*rows = 0),
+ * PP_ERR_INVALID, PP_ERR_CUDA. */
+pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* out_nodes,
+                        int32_t* rows, void* consumer_stream);
+
+/* Assemble the next n steps in ONE launch: step i goes to
+ * out + i*out_stride_bytes (and labels/nodes + i*B elements when non-NULL);
+ * rows[i] receives its row count.  Stops early at the end of the epoch
+ * (*n_done < n).  Same semantics as n calls of pp_next_batch; a k-slot ring
+ * of prefetched batches.  Errors as pp_next_batch (PP_END_OF_EPOCH only if
+ * no step remains). */
+pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes,
+                          int32_t* out_labels, int64_t* out_nodes, int32_t* rows,
+                          int32_t* n_done, void* consumer_stream);
+
+/* Move the cursor to step t (0 <= t <= steps_per_epoch): resume support.
+ * (seed, chunk, cursor) is the loader's whole epoch state. */
+pp_status pp_seek(pp_loader* L, int64_t step);
+
+/* Use `stream` as the loader stream (default: a library-created non-blocking
+ * stream).  When consumer_stream == loader stream, no events are recorded. */
+pp_status pp_set_stream(pp_loader* L, void* stream);
+
+pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* pp_last_error(void);
+
+int32_t pp_abi_version(void);
+
+/* Bytes of the expanded PP-GNN input: N * F * elem_bytes * num_ops * (R + 1)
+ * ("the input feature size is expanded to K(R+1) times"). */
+int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_bytes,
+                           int32_t num_ops, int32_t num_hops_R);
+
+/* ---- multi-GPU plumbing (W > 1) ------------------------------------------ */
+
+/* PP_PEERS_IPC: write this rank's store handle (64 opaque bytes) to
+ * handle_out; the caller all-gathers the W handles (e.g. torch.distributed)
+ * and passes them, rank-ordered, to pp_import_peer_stores on every rank. */
+pp_status pp_export_store(pp_loader* L, void* handle_out);
+pp_status pp_import_peer_stores(pp_loader* L, const void* handles /* W*64 bytes */);
+
+/* PP_PEERS_LOOPBACK: link W handles of one process (same device), rank-ordered. */
+pp_status pp_link_loopback(pp_loader* const* loaders, int32_t world_size);
+
+/* ---- test / bench only ---------------------------------------------------- */
+
+/* Fill this rank's store in place with the §8(d) generator (G for F32, G16
+ * for F16): elem(k, v, f) is a pure function of (data_seed, k, v, f), v the
+ * GLOBAL node id.  Synchronous. */
+pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed);
+
+/* Copy the current epoch's order as global node ids (int64, N entries, after
+ * node-set mapping) to host memory.  Synchronous.  PP_ERR_STATE before the
+ * first permute. */
+pp_status pp_get_order(pp_loader* L, int64_t* dst_host);
+
+/* Copy store rows [row0, row0+n) of this rank (local row ids, node-major
+ * records of record_bytes_in each) to host memory.  Synchronous. */
+pp_status pp_read_store(pp_loader* L, int64_t row0, int64_t n, void* dst_host);
+
+/* Test knob: shift the permutation's bucket count by `delta` bits (negative
+ * = fewer, larger buckets) so the large-bucket path is exercised. */
+pp_status pp_debug_set_sort_bits_delta(pp_loader* L, int32_t delta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PP_LOADER_H */

@@ -1,0 +1,254 @@
+"""B200-native PP-GNN mini-batch loader (arXiv 2504.13266), Python binding.
+
+Argument marshalling over ``libppload.so`` (include/pp_loader.h) with the
+same entry-point names; every step of the loading path runs in the library's
+sm_100a kernels.  There is no CPU fallback: importing the binding without the
+built library raises.
+
+PyTorch is used only for device memory and streams (callers pass tensors /
+``torch.cuda.Stream`` objects; we pass their raw pointers through).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._abi import (  # noqa: F401
+    PP_OK, PP_ERR_INVALID, PP_ERR_OOM, PP_ERR_CUDA, PP_ERR_NCCL, PP_ERR_STATE, PP_END_OF_EPOCH,
+    PP_F32, PP_BF16, PP_F16, PP_MEM_HOST, PP_MEM_DEVICE, PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK,
+    pp_hop_desc, pp_loader_desc, pp_loader_info, PPError, lib, LIB_PATH,
+)
+
+__all__ = [
+    "Loader", "PPError", "lib", "LIB_PATH",
+    "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_next_batch", "pp_next_batches",
+    "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
+    "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
+    "pp_import_peer_stores", "pp_debug_set_sort_bits_delta",
+]
+
+
+def _check(rc: int, what: str, ok=(PP_OK,)) -> int:
+    if rc not in ok:
+        raise PPError(rc, f"{what}: {lib().pp_last_error().decode()}")
+    return rc
+
+
+def _ptr(x) -> int | None:
+    """Raw address of a torch tensor / numpy array / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+_DT = {"f32": PP_F32, "float32": PP_F32, "bf16": PP_BF16, "bfloat16": PP_BF16, "f16": PP_F16, "float16": PP_F16}
+
+
+def _dtype(d) -> int:
+    if isinstance(d, int):
+        return d
+    return _DT[str(d).replace("torch.", "")]
+
+
+# --------------------------------------------------------------------------- same-name entry points
+def pp_abi_version() -> int:
+    return lib().pp_abi_version()
+
+
+def pp_last_error() -> str:
+    return lib().pp_last_error().decode()
+
+
+def pp_footprint_bytes(num_nodes, feat_dim, elem_bytes, num_ops, num_hops_R) -> int:
+    return lib().pp_footprint_bytes(num_nodes, feat_dim, elem_bytes, num_ops, num_hops_R)
+
+
+def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_dim, hop_stride=0, row_stride=0,
+                     dtype=PP_F32, node_set=None, labels=None, batch_size, out_dtype=PP_BF16, drop_last=False,
+                     hbm_budget_bytes=0, world_size=1, rank=0, peers=PP_PEERS_NONE, device=0):
+    """pp_loader_create(desc) -> handle.  ``data`` is a numpy array (host) or a torch CUDA tensor
+    (device) of the hop matrices with the given element strides; None allocates the store only."""
+    d = pp_loader_desc()
+    keep = []
+    if data is not None:
+        if isinstance(data, np.ndarray):
+            data = np.ascontiguousarray(data)
+            keep.append(data)
+            where = PP_MEM_HOST
+        else:
+            where = PP_MEM_DEVICE if data.is_cuda else PP_MEM_HOST
+        d.hops.data = _ptr(data)
+    d.hops.where = where
+    d.hops.num_nodes = num_nodes
+    d.hops.num_hops = num_hops
+    d.hops.feat_dim = feat_dim
+    d.hops.hop_stride = hop_stride
+    d.hops.row_stride = row_stride
+    d.hops.dtype = _dtype(dtype)
+    if node_set is not None:
+        ns = np.ascontiguousarray(node_set, dtype=np.int64)
+        keep.append(ns)
+        d.node_set = ctypes.cast(ns.ctypes.data, ctypes.POINTER(ctypes.c_int64))
+        d.num_set = ns.shape[0]
+    if labels is not None:
+        lab = np.ascontiguousarray(labels, dtype=np.int32)
+        keep.append(lab)
+        d.labels = ctypes.cast(lab.ctypes.data, ctypes.POINTER(ctypes.c_int32))
+    d.batch_size = batch_size
+    d.out_dtype = _dtype(out_dtype)
+    d.drop_last = int(drop_last)
+    d.hbm_budget_bytes = hbm_budget_bytes
+    d.world_size = world_size
+    d.rank = rank
+    d.peers = peers
+    d.device = device
+    h = ctypes.c_void_p()
+    _check(lib().pp_loader_create(ctypes.byref(d), ctypes.byref(h)), "pp_loader_create")
+    return h
+
+
+def pp_loader_destroy(h) -> None:
+    _check(lib().pp_loader_destroy(h), "pp_loader_destroy")
+
+
+def pp_epoch_permute(h, seed: int, chunk: int = 1, stream=None) -> None:
+    _check(lib().pp_epoch_permute(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk, _stream(stream)), "pp_epoch_permute")
+
+
+def pp_next_batch(h, out, out_labels=None, out_nodes=None, consumer_stream=None) -> int:
+    """Returns the rows written, or -1 at the end of the epoch (PP_END_OF_EPOCH)."""
+    rows = ctypes.c_int32()
+    rc = lib().pp_next_batch(h, _ptr(out), _ptr(out_labels), _ptr(out_nodes), ctypes.byref(rows),
+                             _stream(consumer_stream))
+    _check(rc, "pp_next_batch", ok=(PP_OK, PP_END_OF_EPOCH))
+    return -1 if rc == PP_END_OF_EPOCH else rows.value
+
+
+def pp_next_batches(h, n, out, out_stride_bytes, out_labels=None, out_nodes=None, consumer_stream=None):
+    """Returns the list of rows per assembled step ([] at the end of the epoch)."""
+    rows = (ctypes.c_int32 * n)()
+    done = ctypes.c_int32()
+    rc = lib().pp_next_batches(h, n, _ptr(out), out_stride_bytes, _ptr(out_labels), _ptr(out_nodes), rows,
+                               ctypes.byref(done), _stream(consumer_stream))
+    _check(rc, "pp_next_batches", ok=(PP_OK, PP_END_OF_EPOCH))
+    return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
+
+
+def pp_seek(h, step: int) -> None:
+    _check(lib().pp_seek(h, step), "pp_seek")
+
+
+def pp_set_stream(h, stream) -> None:
+    _check(lib().pp_set_stream(h, _stream(stream)), "pp_set_stream")
+
+
+def pp_loader_query(h) -> dict:
+    info = pp_loader_info()
+    _check(lib().pp_loader_query(h, ctypes.byref(info)), "pp_loader_query")
+    return {name: getattr(info, name) for name, _ in pp_loader_info._fields_}
+
+
+def pp_fill_synthetic(h, data_seed: int) -> None:
+    _check(lib().pp_fill_synthetic(h, ctypes.c_uint64(data_seed)), "pp_fill_synthetic")
+
+
+def pp_get_order(h) -> np.ndarray:
+    n = pp_loader_query(h)["num_positions"]
+    out = np.zeros(n, dtype=np.int64)
+    _check(lib().pp_get_order(h, out.ctypes.data), "pp_get_order")
+    return out
+
+
+def pp_read_store(h, row0: int, n: int) -> np.ndarray:
+    q = pp_loader_query(h)
+    out = np.zeros((n, q["record_bytes_in"]), dtype=np.uint8)
+    _check(lib().pp_read_store(h, row0, n, out.ctypes.data), "pp_read_store")
+    return out
+
+
+def pp_link_loopback(handles) -> None:
+    arr = (ctypes.c_void_p * len(handles))(*[h.value for h in handles])
+    _check(lib().pp_link_loopback(arr, len(handles)), "pp_link_loopback")
+
+
+def pp_export_store(h) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().pp_export_store(h, buf), "pp_export_store")
+    return buf.raw
+
+
+def pp_import_peer_stores(h, handles: bytes) -> None:
+    _check(lib().pp_import_peer_stores(h, handles), "pp_import_peer_stores")
+
+
+def pp_debug_set_sort_bits_delta(h, delta: int) -> None:
+    _check(lib().pp_debug_set_sort_bits_delta(h, delta), "pp_debug_set_sort_bits_delta")
+
+
+# --------------------------------------------------------------------------- convenience handle
+class Loader:
+    """Owning wrapper around a ``pp_loader*`` (marshalling only)."""
+
+    def __init__(self, **desc):
+        self.h = pp_loader_create(**desc)
+        self.info = pp_loader_query(self.h)
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            pp_loader_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def epoch_permute(self, seed, chunk=1, stream=None):
+        pp_epoch_permute(self.h, seed, chunk, stream)
+
+    def next_batch(self, out, out_labels=None, out_nodes=None, consumer_stream=None):
+        return pp_next_batch(self.h, out, out_labels, out_nodes, consumer_stream)
+
+    def next_batches(self, n, out, out_stride_bytes, out_labels=None, out_nodes=None, consumer_stream=None):
+        return pp_next_batches(self.h, n, out, out_stride_bytes, out_labels, out_nodes, consumer_stream)
+
+    def seek(self, step):
+        pp_seek(self.h, step)
+
+    def set_stream(self, stream):
+        pp_set_stream(self.h, stream)
+
+    def query(self):
+        return pp_loader_query(self.h)
+
+    def fill_synthetic(self, data_seed):
+        pp_fill_synthetic(self.h, data_seed)
+
+    def get_order(self):
+        return pp_get_order(self.h)
+
+    def read_store(self, row0, n):
+        return pp_read_store(self.h, row0, n)

@@ -1,0 +1,287 @@
+// Batch assembly kernels (K3/K5/K6 of §2.3).
+//
+// out[j, k, f] = cast(X_k[v_j, f]),  v_j = S[order[p_j]]  (oracle O8-O10)
+// "copy the scattered node features" of a batch into one contiguous tensor
+// (PAPER.md:259), done on the GPU with the fp32 -> bf16/fp16 RNE cast fused.
+//
+// B200 design.
+//   * The store is node-major [rows, H, F]: one node's K+1 hop vectors are one
+//     contiguous record (1600 B for ogbn-products fp32), so a batch row is a
+//     single streaming copy instead of H scattered ones.
+//   * A CTA takes a tile of 32 batch rows.  Threads 0..31 resolve the rows
+//     (order -> node set -> owner shard -> HBM or pinned-host record) once and
+//     park the 32 source pointers in shared memory; all 256 threads then sweep
+//     the tile's rows x (record / 32 B) vector slots flattened, so every lane
+//     works even when a record is not a multiple of 32 vectors (50 for
+//     products).  Loads are 128-bit, read-only, L1-no-allocate, four slots per
+//     thread issued before any store (~64 KB in flight per SM).
+//   * Rows past the HBM budget are read from pinned, mapped host memory with
+//     the same instructions (UVA zero-copy over PCIe, K6).  Sharded loaders
+//     read the owner's store through a peer pointer (NVLink loads, A5).
+//   * Casts use cvt.rn.{bf16x2,f16x2}.f32 (round to nearest even).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "philox.cuh"
+
+namespace ppl {
+
+constexpr int kTileRows = 32;
+constexpr int kGatherThreads = 256;
+constexpr int kUnroll = 4;
+
+enum { kF32 = 0, kBF16 = 1, kF16 = 2 };
+enum { kModeBF16 = 0, kModeF16 = 1, kModeCopy = 2 };
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_vec(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack_f16(uint32_t lo, uint32_t hi) {
+  const __half2 h = __floats2half2_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// e / d for e * d < 2^40 with M = ceil(2^40 / d)
+__device__ __forceinline__ uint32_t fast_div(uint32_t e, uint64_t M) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(e) * M) >> 40);
+}
+
+// Resolve the tile's rows (threads 0..rows-1): source record pointer into
+// shared memory, labels / node ids out.
+template <bool SHARDED>
+__device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, int64_t step_pos, int j0,
+                                             int rows, const uint8_t** s_src) {
+  if (threadIdx.x < rows) {
+    const int64_t p = step_pos + j0 + threadIdx.x;
+    uint64_t v = a.order[p];
+    if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
+    int owner = 0;
+    uint64_t lr = v;
+    if (SHARDED) {
+      owner = static_cast<int>(v % static_cast<uint64_t>(a.W));
+      lr = v / static_cast<uint64_t>(a.W);
+    }
+    const ShardView sh = a.shards[owner];
+    const int64_t l = static_cast<int64_t>(lr);
+    s_src[threadIdx.x] = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
+    const int64_t oj = step * a.B + j0 + threadIdx.x;
+    if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
+    if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
+  }
+}
+
+// Vector path: MODE bf16/f16 reads 32 B (8 fp32) and writes 16 B; copy mode
+// moves 16 B.  vpr = vector slots per row.
+template <int MODE, bool SHARDED>
+__global__ void __launch_bounds__(kGatherThreads) k_gather_vec(const GatherArgs a, uint32_t vpr, uint64_t vpr_M,
+                                                               int64_t row_out_bytes) {
+  __shared__ const uint8_t* s_src[2][kTileRows];
+  constexpr int kInBytes = (MODE == kModeCopy) ? 16 : 32;
+  const int64_t tiles_per_step = (a.B + kTileRows - 1) / kTileRows;
+  const int64_t total_tiles = tiles_per_step * a.nsteps;
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const int64_t step = tile / tiles_per_step;
+    const int j0 = static_cast<int>(tile - step * tiles_per_step) * kTileRows;
+    const int64_t step_pos = a.first_pos + step * a.step_stride;
+    const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
+    const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), nrows_step - j0));
+    if (rows <= 0) continue;  // block-uniform; buf is not toggled
+    resolve_rows<SHARDED>(a, step, step_pos, j0, rows, s_src[buf]);
+    __syncthreads();
+    uint8_t* out_tile = a.out + step * a.out_stride + static_cast<int64_t>(j0) * row_out_bytes;
+    const uint32_t nvec = static_cast<uint32_t>(rows) * vpr;
+    for (uint32_t e0 = threadIdx.x; e0 < nvec; e0 += kGatherThreads * kUnroll) {
+      uint4 x0[kUnroll], x1[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint32_t e = e0 + q * kGatherThreads;
+        if (e < nvec) {
+          const uint32_t r = fast_div(e, vpr_M);
+          const uint32_t c = e - r * vpr;
+          const uint8_t* src = s_src[buf][r] + static_cast<int64_t>(c) * kInBytes;
+          x0[q] = ld_stream(src);
+          if (MODE != kModeCopy) x1[q] = ld_stream(src + 16);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const uint32_t e = e0 + q * kGatherThreads;
+        if (e < nvec) {
+          const uint32_t r = fast_div(e, vpr_M);
+          const uint32_t c = e - r * vpr;
+          uint8_t* dst = out_tile + static_cast<int64_t>(r) * row_out_bytes + static_cast<int64_t>(c) * 16;
+          uint4 y;
+          if (MODE == kModeBF16) {
+            y = make_uint4(pack_bf16(x0[q].x, x0[q].y), pack_bf16(x0[q].z, x0[q].w), pack_bf16(x1[q].x, x1[q].y),
+                           pack_bf16(x1[q].z, x1[q].w));
+          } else if (MODE == kModeF16) {
+            y = make_uint4(pack_f16(x0[q].x, x0[q].y), pack_f16(x0[q].z, x0[q].w), pack_f16(x1[q].x, x1[q].y),
+                           pack_f16(x1[q].z, x1[q].w));
+          } else {
+            y = x0[q];
+          }
+          st_vec(dst, y);
+        }
+      }
+    }
+    buf ^= 1;
+  }
+}
+
+// Scalar fallback for records whose size / alignment rule out the vector
+// path.  Same tile structure, one element per slot.
+template <bool SHARDED>
+__global__ void __launch_bounds__(kGatherThreads) k_gather_scalar(const GatherArgs a, uint32_t HF, uint64_t HF_M) {
+  __shared__ const uint8_t* s_src[2][kTileRows];
+  const int s_in = a.in_dtype == kF32 ? 4 : 2;
+  const int s_out = a.out_dtype == kF32 ? 4 : 2;
+  const int64_t row_out_bytes = static_cast<int64_t>(HF) * s_out;
+  const int64_t tiles_per_step = (a.B + kTileRows - 1) / kTileRows;
+  const int64_t total_tiles = tiles_per_step * a.nsteps;
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const int64_t step = tile / tiles_per_step;
+    const int j0 = static_cast<int>(tile - step * tiles_per_step) * kTileRows;
+    const int64_t step_pos = a.first_pos + step * a.step_stride;
+    const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
+    const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), nrows_step - j0));
+    if (rows <= 0) continue;
+    resolve_rows<SHARDED>(a, step, step_pos, j0, rows, s_src[buf]);
+    __syncthreads();
+    uint8_t* out_tile = a.out + step * a.out_stride + static_cast<int64_t>(j0) * row_out_bytes;
+    const uint32_t nel = static_cast<uint32_t>(rows) * HF;
+    for (uint32_t e = threadIdx.x; e < nel; e += kGatherThreads) {
+      const uint32_t r = fast_div(e, HF_M);
+      const uint32_t i = e - r * HF;
+      const uint8_t* src = s_src[buf][r] + static_cast<int64_t>(i) * s_in;
+      uint8_t* dst = out_tile + static_cast<int64_t>(r) * row_out_bytes + static_cast<int64_t>(i) * s_out;
+      if (s_in == 4) {
+        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
+        if (a.out_dtype == kBF16) {
+          const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(x));
+          *reinterpret_cast<__nv_bfloat16*>(dst) = h;
+        } else if (a.out_dtype == kF16) {
+          const __half h = __float2half_rn(__uint_as_float(x));
+          *reinterpret_cast<__half*>(dst) = h;
+        } else {
+          *reinterpret_cast<uint32_t*>(dst) = x;
+        }
+      } else {
+        *reinterpret_cast<uint16_t*>(dst) = __ldg(reinterpret_cast<const unsigned short*>(src));
+      }
+    }
+    buf ^= 1;
+  }
+}
+
+bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride) {
+  const int s_in = in_dtype == kF32 ? 4 : 2;
+  const int s_out = out_dtype == kF32 ? 4 : 2;
+  const int64_t in_row = static_cast<int64_t>(HF) * s_in, out_row = static_cast<int64_t>(HF) * s_out;
+  if (rec_stride % 16 != 0 || out_row % 16 != 0) return false;
+  if (s_in == s_out) return in_row % 16 == 0;
+  return in_row % 32 == 0;  // fp32 -> 16-bit: 8 elements per slot
+}
+
+cudaError_t launch_gather(const GatherArgs& a, bool vector_path, cudaStream_t st) {
+  const int64_t tiles = ((a.B + kTileRows - 1) / kTileRows) * static_cast<int64_t>(a.nsteps);
+  if (tiles <= 0) return cudaSuccess;
+  const int64_t grid = tiles < 148 * 8 ? tiles : 148 * 8;  // 8 resident 256-thread CTAs per SM
+  const bool sharded = a.W > 1;
+  const int s_out = a.out_dtype == kF32 ? 4 : 2;
+  if (vector_path) {
+    const int mode = (a.in_dtype == a.out_dtype) ? kModeCopy : (a.out_dtype == kBF16 ? kModeBF16 : kModeF16);
+    const int64_t row_out_bytes = static_cast<int64_t>(a.HF) * s_out;
+    const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
+    const uint64_t M = ((1ull << 40) + vpr - 1) / vpr;
+    if (static_cast<uint64_t>(kTileRows) * vpr * vpr >= (1ull << 40)) return cudaErrorInvalidValue;
+#define PPL_GV(MODE, SH) k_gather_vec<MODE, SH><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, vpr, M, row_out_bytes)
+    if (mode == kModeBF16) { if (sharded) PPL_GV(kModeBF16, true); else PPL_GV(kModeBF16, false); }
+    else if (mode == kModeF16) { if (sharded) PPL_GV(kModeF16, true); else PPL_GV(kModeF16, false); }
+    else { if (sharded) PPL_GV(kModeCopy, true); else PPL_GV(kModeCopy, false); }
+#undef PPL_GV
+  } else {
+    const uint32_t HF = static_cast<uint32_t>(a.HF);
+    if (static_cast<uint64_t>(kTileRows) * HF * HF >= (1ull << 40)) return cudaErrorInvalidValue;
+    const uint64_t M = ((1ull << 40) + HF - 1) / HF;
+    if (sharded)
+      k_gather_scalar<true><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, HF, M);
+    else
+      k_gather_scalar<false><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, HF, M);
+  }
+  return cudaGetLastError();
+}
+
+// ---- K10: synthetic fill (SURVEY.md §8(d) generators G / G16) ----------------
+__global__ void k_fill_synthetic(uint8_t* __restrict__ base, int64_t row0, int64_t nrows, int64_t rec_stride,
+                                 int32_t H, int32_t F, int32_t dtype, uint64_t seed, int32_t W, int32_t rank) {
+  const int32_t F4 = (F + 3) / 4;
+  const int64_t total = nrows * H * F4;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = t / (static_cast<int64_t>(H) * F4);
+    const int32_t rem = static_cast<int32_t>(t - row * H * F4);
+    const int32_t k = rem / F4;
+    const int32_t f4 = rem - k * F4;
+    const uint64_t v = static_cast<uint64_t>(row0 + row) * W + rank;  // global node id
+    const uint4 w4 = synth_block(seed, v, static_cast<uint32_t>(k), static_cast<uint32_t>(f4));
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+    uint8_t* rec = base + row * rec_stride;
+    for (int q = 0; q < 4; ++q) {
+      const int32_t f = f4 * 4 + q;
+      if (f >= F) break;
+      if (dtype == kF32) {
+        const uint32_t bits = (w[q] & 0x807FFFFFu) | ((120u + ((w[q] >> 23) & 15u)) << 23);
+        reinterpret_cast<uint32_t*>(rec)[static_cast<int64_t>(k) * F + f] = bits;
+      } else {
+        const uint16_t h = static_cast<uint16_t>((w[q] & 0x83FFu) | ((8u + ((w[q] >> 10) & 15u)) << 10));
+        reinterpret_cast<uint16_t*>(rec)[static_cast<int64_t>(k) * F + f] = h;
+      }
+    }
+  }
+}
+
+cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
+                                  int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,
+                                  cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  k_fill_synthetic<<<148 * 16, 256, 0, st>>>(base, row0, nrows, rec_stride, H, F, dtype, data_seed, W, rank);
+  return cudaGetLastError();
+}
+
+__global__ void k_order_to_nodes(const uint32_t* __restrict__ order, const int64_t* __restrict__ node_set,
+                                 int64_t N, int64_t* __restrict__ dst) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < N;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t i = order[p];
+    dst[p] = node_set != nullptr ? node_set[i] : static_cast<int64_t>(i);
+  }
+}
+
+cudaError_t launch_order_to_nodes(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t* dst,
+                                  cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  k_order_to_nodes<<<148 * 8, 256, 0, st>>>(order, node_set, N, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace ppl

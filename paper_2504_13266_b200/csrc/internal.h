@@ -1,0 +1,77 @@
+// Internal interfaces between the C-ABI host code (pp_loader.cu) and the
+// sm_100a kernels (permute.cu, gather.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ppl {
+
+constexpr int kMaxWorld = 8;
+
+// Where the rows owned by one rank live: local row lr < n_hbm at
+// hbm + lr * rec_stride, otherwise at spill + (lr - n_hbm) * rec_stride
+// (spill = device alias of pinned, mapped host memory: UVA zero-copy).
+struct ShardView {
+  const uint8_t* hbm;
+  const uint8_t* spill;
+  int64_t n_hbm;
+};
+
+// ---- permutation (permute.cu) ------------------------------------------------
+struct SortScratch {
+  uint32_t* counts;     // [nb + 1]  bucket histogram, then exclusive offsets
+  uint32_t* cursor;     // [nb]      scatter cursors
+  uint32_t* blocksums;  // [ceil((nb+1)/kScanTile)]
+  uint32_t* tmp;        // [U]       unit ids grouped by bucket
+  uint32_t* ragged;     // [1]       position of the ragged chunk in pi
+};
+constexpr int kScanTile = 4096;
+
+// Buckets used for U units: 2^bits with U / 2^bits in ~[14, 28).
+int sort_bucket_bits(uint64_t U, int delta);
+
+// pi[0..U) = units sorted by (Philox key, unit id).  All on `st`.
+cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, const SortScratch& s, uint32_t* pi,
+                                    cudaStream_t st);
+
+// order[p], p in [0, N): chunk expansion of pi (chunk c, U = ceil(N / c)).
+cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, uint32_t* ragged,
+                                uint32_t* order, cudaStream_t st);
+
+// ---- batch assembly (gather.cu) ----------------------------------------------
+struct GatherArgs {
+  const uint32_t* order;    // positions -> index into node set (or node id)
+  const int64_t* node_set;  // may be null
+  const int32_t* labels;    // may be null
+  int64_t N;                // positions in an epoch
+  int64_t first_pos;        // first position of this rank in the first step
+  int64_t step_stride;      // W * B
+  int32_t B;
+  int32_t nsteps;
+  uint8_t* out;
+  int64_t out_stride;       // bytes between step slots
+  int32_t* out_labels;      // [nsteps * B] or null
+  int64_t* out_nodes;       // [nsteps * B] or null
+  int32_t W;
+  ShardView shards[kMaxWorld];
+  int64_t rec_stride;       // store pitch (bytes)
+  int32_t HF;               // elements per record
+  int32_t in_dtype, out_dtype;  // pp_dtype codes
+};
+
+// Returns cudaErrorInvalidValue when the vector path's alignment rules are
+// not met and `allow_scalar` is false.
+cudaError_t launch_gather(const GatherArgs& a, bool vector_path, cudaStream_t st);
+bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride);
+
+// ---- synthetic fill (gather.cu) ---------------------------------------------
+cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
+                                  int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,
+                                  cudaStream_t st);
+
+// order (u32 positions) -> global node ids (int64), for pp_get_order.
+cudaError_t launch_order_to_nodes(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t* dst,
+                                  cudaStream_t st);
+
+}  // namespace ppl

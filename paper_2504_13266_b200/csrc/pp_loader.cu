@@ -1,0 +1,558 @@
+// C-ABI implementation of libppload.so (include/pp_loader.h).
+//
+// Owns: the node-major hop store (HBM part + pinned/mapped host spill), the
+// uploaded node set and labels, the epoch order and sort scratch, the loader
+// stream and its events, and peer store mappings.  All compute is in the
+// kernels of permute.cu / gather.cu; this file validates, allocates, lays out
+// and enqueues.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pp_loader.h"
+#include "internal.h"
+
+using namespace ppl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pp_status fail(pp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+int elem_bytes(pp_dtype d) { return d == PP_F32 ? 4 : 2; }
+bool valid_dtype(int d) { return d == PP_F32 || d == PP_BF16 || d == PP_F16; }
+
+struct DevGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct pp_loader {
+  pp_loader_desc desc{};
+  int dev = 0;
+  int32_t W = 1, rank = 0, H = 0, F = 0, HF = 0;
+  pp_dtype in_dtype = PP_F32, out_dtype = PP_BF16;
+  int64_t N_total = 0, N = 0, B = 0, local_rows = 0, n_hbm = 0, n_spill = 0;
+  int64_t rec_in = 0, rec_stride = 0, rec_out = 0, steps = 0;
+  bool vector_path = true;
+
+  uint8_t* d_store = nullptr;
+  uint8_t* h_spill = nullptr;
+  uint8_t* d_spill = nullptr;  // device alias of h_spill
+  int64_t* d_node_set = nullptr;
+  int32_t* d_labels = nullptr;
+  bool has_labels = false;
+
+  uint32_t* d_order = nullptr;
+  uint32_t* d_pi = nullptr;
+  int64_t pi_cap = 0;
+  SortScratch sort{};
+  int sort_bits_max = 0;
+  int sort_bits_delta = 0;
+
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+
+  ShardView shards[kMaxWorld]{};
+  bool linked = false;
+  std::vector<void*> ipc_opened;
+
+  bool permuted = false, poisoned = false;
+  uint64_t seed = 0;
+  int64_t chunk = 1, cursor = 0;
+};
+
+namespace {
+
+pp_status cuda_fail(pp_loader* L, cudaError_t e, const char* what) {
+  if (L) L->poisoned = true;
+  return fail(PP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define PPL_CUDA(L, call)                                  \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) return cuda_fail((L), _e, #call); \
+  } while (0)
+
+void release(pp_loader* L) {
+  if (!L) return;
+  if (L->stream) cudaStreamSynchronize(L->stream);
+  for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(L->d_store);
+  if (L->h_spill) cudaFreeHost(L->h_spill);
+  cudaFree(L->d_node_set);
+  cudaFree(L->d_labels);
+  cudaFree(L->d_order);
+  cudaFree(L->d_pi);
+  cudaFree(L->sort.counts);
+  cudaFree(L->sort.cursor);
+  cudaFree(L->sort.blocksums);
+  cudaFree(L->sort.tmp);
+  cudaFree(L->sort.ragged);
+  if (L->ev_in) cudaEventDestroy(L->ev_in);
+  if (L->ev_out) cudaEventDestroy(L->ev_out);
+  if (L->own_stream && L->stream) cudaStreamDestroy(L->stream);
+  delete L;
+}
+
+// Copy rows [row0, row0 + n) of this rank's slice (global rows v = lr*W + r)
+// of every hop into dst (record pitch rec_stride), strided 2-D copies.
+cudaError_t copy_in(const pp_loader* L, const pp_hop_desc& h, int64_t row0, int64_t n, uint8_t* dst) {
+  const int s = elem_bytes(h.dtype);
+  const uint8_t* src = static_cast<const uint8_t*>(h.data);
+  const size_t spitch = static_cast<size_t>(h.row_stride) * L->W * s;
+  const int64_t kMaxRows = 1 << 22;
+  for (int32_t k = 0; k < L->H; ++k) {
+    for (int64_t a = 0; a < n; a += kMaxRows) {
+      const int64_t m = std::min(kMaxRows, n - a);
+      const int64_t lr = row0 + a;
+      const int64_t v = lr * L->W + L->rank;
+      const uint8_t* s0 = src + (static_cast<int64_t>(k) * h.hop_stride + v * h.row_stride) * s;
+      uint8_t* d0 = dst + a * L->rec_stride + static_cast<int64_t>(k) * L->F * s;
+      cudaError_t e = cudaMemcpy2D(d0, L->rec_stride, s0, spitch, static_cast<size_t>(L->F) * s, m, cudaMemcpyDefault);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+pp_status validate(const pp_loader_desc* d) {
+  if (!d) return fail(PP_ERR_INVALID, "desc is NULL");
+  const pp_hop_desc& h = d->hops;
+  if (h.num_nodes < 1 || h.num_nodes >= (int64_t(1) << 32))
+    return fail(PP_ERR_INVALID, "num_nodes must be in [1, 2^32), got %lld", (long long)h.num_nodes);
+  if (h.num_hops < 1 || h.feat_dim < 1) return fail(PP_ERR_INVALID, "num_hops and feat_dim must be >= 1");
+  if (static_cast<int64_t>(h.num_hops) * h.feat_dim >= (int64_t(1) << 24))
+    return fail(PP_ERR_INVALID, "H*F too large");
+  if (!valid_dtype(h.dtype) || !valid_dtype(d->out_dtype)) return fail(PP_ERR_INVALID, "unknown dtype");
+  if (h.where != PP_MEM_HOST && h.where != PP_MEM_DEVICE) return fail(PP_ERR_INVALID, "unknown memory kind");
+  const bool cast = h.dtype == PP_F32 && (d->out_dtype == PP_BF16 || d->out_dtype == PP_F16);
+  if (!cast && h.dtype != d->out_dtype)
+    return fail(PP_ERR_INVALID, "unsupported dtype pair (store %d -> out %d)", h.dtype, d->out_dtype);
+  if (h.data) {
+    if (h.row_stride < h.feat_dim || h.hop_stride < 0)
+      return fail(PP_ERR_INVALID, "row_stride must be >= feat_dim and hop_stride >= 0");
+  }
+  if (d->batch_size < 1) return fail(PP_ERR_INVALID, "batch_size must be >= 1");
+  if (d->world_size < 1 || d->world_size > kMaxWorld)
+    return fail(PP_ERR_INVALID, "world_size must be in [1, %d]", kMaxWorld);
+  if (d->rank < 0 || d->rank >= d->world_size) return fail(PP_ERR_INVALID, "rank out of range");
+  if ((d->world_size == 1) != (d->peers == PP_PEERS_NONE))
+    return fail(PP_ERR_INVALID, "peers must be PP_PEERS_NONE iff world_size == 1");
+  if (d->peers != PP_PEERS_NONE && d->peers != PP_PEERS_IPC && d->peers != PP_PEERS_LOOPBACK)
+    return fail(PP_ERR_INVALID, "unknown peers mode");
+  if (d->node_set) {
+    if (d->num_set < 1 || d->num_set >= (int64_t(1) << 32)) return fail(PP_ERR_INVALID, "num_set out of range");
+    for (int64_t i = 0; i < d->num_set; ++i)
+      if (d->node_set[i] < 0 || d->node_set[i] >= h.num_nodes)
+        return fail(PP_ERR_INVALID, "node_set[%lld] = %lld out of range", (long long)i, (long long)d->node_set[i]);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || d->device < 0 || d->device >= ndev)
+    return fail(PP_ERR_INVALID, "device %d not available", d->device);
+  return PP_OK;
+}
+
+pp_status ensure_sort_scratch(pp_loader* L, uint32_t U, int bits) {
+  if (bits > L->sort_bits_max || !L->sort.counts) {
+    const int nbits = std::max(bits, L->sort_bits_max);
+    cudaFree(L->sort.counts);
+    cudaFree(L->sort.cursor);
+    cudaFree(L->sort.blocksums);
+    L->sort.counts = L->sort.cursor = L->sort.blocksums = nullptr;
+    const size_t nb = size_t(1) << nbits;
+    const size_t nblk = (nb + 1 + kScanTile - 1) / kScanTile;
+    if (cudaMalloc(&L->sort.counts, (nb + 1) * 4) != cudaSuccess || cudaMalloc(&L->sort.cursor, nb * 4) != cudaSuccess ||
+        cudaMalloc(&L->sort.blocksums, nblk * 4) != cudaSuccess)
+      return fail(PP_ERR_OOM, "sort scratch allocation failed (2^%d buckets)", nbits);
+    L->sort_bits_max = nbits;
+  }
+  (void)U;
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pp_abi_version(void) { return PP_ABI_VERSION; }
+
+const char* pp_last_error(void) { return g_last_error.c_str(); }
+
+int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_bytes_, int32_t num_ops,
+                           int32_t num_hops_R) {
+  if (num_nodes < 0 || feat_dim < 0 || elem_bytes_ < 0 || num_ops < 0 || num_hops_R < 0) return -1;
+  return num_nodes * feat_dim * elem_bytes_ * static_cast<int64_t>(num_ops) * (num_hops_R + 1);
+}
+
+pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
+  if (!out) return fail(PP_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  pp_status st = validate(desc);
+  if (st != PP_OK) return st;
+  DevGuard g(desc->device);
+  if (!g.ok) return fail(PP_ERR_CUDA, "cudaSetDevice(%d) failed", desc->device);
+
+  pp_loader* L = new (std::nothrow) pp_loader();
+  if (!L) return fail(PP_ERR_OOM, "host allocation failed");
+  L->desc = *desc;
+  L->desc.node_set = nullptr;
+  L->desc.labels = nullptr;
+  L->desc.hops.data = nullptr;
+  L->dev = desc->device;
+  L->W = desc->world_size;
+  L->rank = desc->rank;
+  L->H = desc->hops.num_hops;
+  L->F = desc->hops.feat_dim;
+  L->HF = L->H * L->F;
+  L->in_dtype = desc->hops.dtype;
+  L->out_dtype = desc->out_dtype;
+  L->N_total = desc->hops.num_nodes;
+  L->N = desc->node_set ? desc->num_set : L->N_total;
+  L->B = desc->batch_size;
+  const int64_t per_step = L->B * L->W;
+  L->steps = desc->drop_last ? L->N / per_step : (L->N + per_step - 1) / per_step;
+  L->local_rows = (L->N_total - L->rank + L->W - 1) / L->W;
+  L->rec_in = static_cast<int64_t>(L->HF) * elem_bytes(L->in_dtype);
+  L->rec_stride = (L->rec_in + 15) / 16 * 16;
+  L->rec_out = static_cast<int64_t>(L->HF) * elem_bytes(L->out_dtype);
+  L->vector_path = gather_vector_ok(L->HF, L->in_dtype, L->out_dtype, L->rec_stride);
+
+  auto bail = [&](pp_status s) {
+    release(L);
+    return s;
+  };
+
+  // ---- placement: HBM budget, remainder spills to pinned mapped host memory
+  const int64_t scratch = L->N * 4 * 3 + (int64_t(1) << 26) + (L->has_labels ? L->N_total * 4 : 0);
+  int64_t budget = desc->hbm_budget_bytes;
+  if (budget == 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return bail(fail(PP_ERR_CUDA, "cudaMemGetInfo failed"));
+    budget = static_cast<int64_t>(fr) - (int64_t(2) << 30) - scratch - L->N_total * 4 - L->N * 8;
+    if (budget < 0) budget = 0;
+  }
+  L->n_hbm = budget < 0 ? 0 : std::min<int64_t>(L->local_rows, budget / L->rec_stride);
+  L->n_spill = L->local_rows - L->n_hbm;
+  if (L->W > 1 && L->n_spill > 0 && desc->peers == PP_PEERS_IPC)
+    return bail(fail(PP_ERR_INVALID, "sharded (IPC) loaders need the whole shard in HBM (%lld rows spill)",
+                     (long long)L->n_spill));
+
+  if (L->n_hbm > 0 && cudaMalloc(&L->d_store, static_cast<size_t>(L->n_hbm * L->rec_stride)) != cudaSuccess)
+    return bail(fail(PP_ERR_OOM, "cudaMalloc of the %lld-byte HBM store failed", (long long)(L->n_hbm * L->rec_stride)));
+  if (L->n_spill > 0) {
+    if (cudaHostAlloc(&L->h_spill, static_cast<size_t>(L->n_spill * L->rec_stride),
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return bail(fail(PP_ERR_OOM, "pinned spill allocation of %lld bytes failed", (long long)(L->n_spill * L->rec_stride)));
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->d_spill), L->h_spill, 0) != cudaSuccess)
+      return bail(fail(PP_ERR_CUDA, "cudaHostGetDevicePointer failed"));
+  }
+  if (desc->hops.data) {
+    cudaError_t e = copy_in(L, desc->hops, 0, L->n_hbm, L->d_store);
+    if (e == cudaSuccess && L->n_spill > 0) e = copy_in(L, desc->hops, L->n_hbm, L->n_spill, L->h_spill);
+    if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
+  }
+  // ---- node set, labels, order, sort scratch
+  if (desc->node_set) {
+    if (cudaMalloc(&L->d_node_set, L->N * 8) != cudaSuccess) return bail(fail(PP_ERR_OOM, "node_set allocation"));
+    if (cudaMemcpy(L->d_node_set, desc->node_set, L->N * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(PP_ERR_CUDA, "node_set upload"));
+  }
+  if (desc->labels) {
+    L->has_labels = true;
+    if (cudaMalloc(&L->d_labels, L->N_total * 4) != cudaSuccess) return bail(fail(PP_ERR_OOM, "labels allocation"));
+    if (cudaMemcpy(L->d_labels, desc->labels, L->N_total * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(PP_ERR_CUDA, "labels upload"));
+  }
+  if (cudaMalloc(&L->d_order, L->N * 4) != cudaSuccess || cudaMalloc(&L->sort.tmp, L->N * 4) != cudaSuccess ||
+      cudaMalloc(&L->sort.ragged, 4) != cudaSuccess)
+    return bail(fail(PP_ERR_OOM, "order / sort scratch allocation"));
+  st = ensure_sort_scratch(L, static_cast<uint32_t>(L->N), sort_bucket_bits(L->N, 0));
+  if (st != PP_OK) return bail(st);
+  if (cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(PP_ERR_CUDA, "stream creation"));
+  L->own_stream = true;
+  if (cudaEventCreateWithFlags(&L->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_out, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(PP_ERR_CUDA, "event creation"));
+  L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
+  L->linked = (L->W == 1);
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PP_ERR_CUDA, "create sync"));
+  *out = L;
+  return PP_OK;
+}
+
+pp_status pp_loader_destroy(pp_loader* L) {
+  if (!L) return PP_OK;
+  DevGuard g(L->dev);
+  release(L);
+  return PP_OK;
+}
+
+pp_status pp_set_stream(pp_loader* L, void* stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  DevGuard g(L->dev);
+  PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+  if (L->own_stream) cudaStreamDestroy(L->stream);
+  L->stream = static_cast<cudaStream_t>(stream);
+  L->own_stream = false;
+  return PP_OK;
+}
+
+pp_status pp_debug_set_sort_bits_delta(pp_loader* L, int32_t delta) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  L->sort_bits_delta = delta;
+  return PP_OK;
+}
+
+pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
+  DevGuard g(L->dev);
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  if (user != L->stream) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, user));
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+  }
+  const uint32_t U = static_cast<uint32_t>((L->N + chunk - 1) / chunk);
+  const int bits = sort_bucket_bits(U, L->sort_bits_delta);
+  pp_status st = ensure_sort_scratch(L, U, bits);
+  if (st != PP_OK) return st;
+  if (chunk == 1) {
+    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort, L->d_order, L->stream));
+  } else {
+    if (L->pi_cap < U) {
+      cudaFree(L->d_pi);
+      L->d_pi = nullptr;
+      if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
+      L->pi_cap = U;
+    }
+    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort, L->d_pi, L->stream));
+    PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(L->N), static_cast<uint64_t>(chunk),
+                                    L->sort.ragged, L->d_order, L->stream));
+  }
+  if (user != L->stream) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+    PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
+  }
+  L->permuted = true;
+  L->seed = seed;
+  L->chunk = chunk;
+  L->cursor = 0;
+  return PP_OK;
+}
+
+static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stride, int32_t* out_labels,
+                            int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (!rows || n < 1) return fail(PP_ERR_INVALID, "rows is NULL or n < 1");
+  if (!L->permuted) return fail(PP_ERR_STATE, "pp_next_batch before pp_epoch_permute");
+  if (!L->linked) return fail(PP_ERR_STATE, "sharded loader: peers not linked yet");
+  if (out_labels && !L->has_labels) return fail(PP_ERR_INVALID, "out_labels given but the loader has no labels");
+  if (L->cursor >= L->steps) {
+    rows[0] = 0;
+    if (n_done) *n_done = 0;
+    return PP_END_OF_EPOCH;
+  }
+  if (!out) return fail(PP_ERR_INVALID, "out is NULL");
+  const int64_t nsteps = std::min<int64_t>(n, L->steps - L->cursor);
+  if (nsteps > 1 && out_stride < L->B * L->rec_out)
+    return fail(PP_ERR_INVALID, "out_stride_bytes %lld < one batch (%lld)", (long long)out_stride,
+                (long long)(L->B * L->rec_out));
+  const bool vec = L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
+  DevGuard g(L->dev);
+  cudaStream_t cons = static_cast<cudaStream_t>(consumer_stream);
+  const bool handoff = cons != L->stream;
+  if (handoff) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+  }
+  GatherArgs a{};
+  a.order = L->d_order;
+  a.node_set = L->d_node_set;
+  a.labels = L->d_labels;
+  a.N = L->N;
+  a.first_pos = L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
+  a.step_stride = L->B * L->W;
+  a.B = static_cast<int32_t>(L->B);
+  a.nsteps = static_cast<int32_t>(nsteps);
+  a.out = static_cast<uint8_t*>(out);
+  a.out_stride = out_stride;
+  a.out_labels = out_labels;
+  a.out_nodes = out_nodes;
+  a.W = L->W;
+  for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = L->shards[i];
+  a.rec_stride = L->rec_stride;
+  a.HF = L->HF;
+  a.in_dtype = L->in_dtype;
+  a.out_dtype = L->out_dtype;
+  PPL_CUDA(L, launch_gather(a, vec, L->stream));
+  if (handoff) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+    PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
+  }
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const int64_t s = a.first_pos + i * a.step_stride;
+    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - s)));
+  }
+  L->cursor += nsteps;
+  if (n_done) *n_done = static_cast<int32_t>(nsteps);
+  return PP_OK;
+}
+
+pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* out_nodes, int32_t* rows,
+                        void* consumer_stream) {
+  return next_steps(L, 1, out, 0, out_labels, out_nodes, rows, nullptr, consumer_stream);
+}
+
+pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes, int32_t* out_labels,
+                          int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
+  return next_steps(L, n, out, out_stride_bytes, out_labels, out_nodes, rows, n_done, consumer_stream);
+}
+
+pp_status pp_seek(pp_loader* L, int64_t step) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (!L->permuted) return fail(PP_ERR_STATE, "pp_seek before pp_epoch_permute");
+  if (step < 0 || step > L->steps) return fail(PP_ERR_INVALID, "step out of range");
+  L->cursor = step;
+  return PP_OK;
+}
+
+pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
+  if (!L || !info) return fail(PP_ERR_INVALID, "NULL argument");
+  info->num_positions = L->N;
+  info->num_nodes_total = L->N_total;
+  info->local_rows = L->local_rows;
+  info->rows_hbm = L->n_hbm;
+  info->rows_spill = L->n_spill;
+  info->record_bytes_in = L->rec_in;
+  info->record_stride = L->rec_stride;
+  info->record_bytes_out = L->rec_out;
+  info->steps_per_epoch = L->steps;
+  info->cursor = L->cursor;
+  info->permuted = L->permuted ? 1 : 0;
+  info->gather_path = L->vector_path ? 0 : 1;
+  return PP_OK;
+}
+
+pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (L->in_dtype == PP_BF16) return fail(PP_ERR_INVALID, "no synthetic generator for bf16 stores");
+  DevGuard g(L->dev);
+  PPL_CUDA(L, launch_fill_synthetic(L->d_store, 0, L->n_hbm, L->rec_stride, L->H, L->F, L->in_dtype, data_seed, L->W,
+                                    L->rank, L->stream));
+  PPL_CUDA(L, launch_fill_synthetic(L->d_spill, L->n_hbm, L->n_spill, L->rec_stride, L->H, L->F, L->in_dtype,
+                                    data_seed, L->W, L->rank, L->stream));
+  PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+  return PP_OK;
+}
+
+pp_status pp_get_order(pp_loader* L, int64_t* dst_host) {
+  if (!L || !dst_host) return fail(PP_ERR_INVALID, "NULL argument");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (!L->permuted) return fail(PP_ERR_STATE, "pp_get_order before pp_epoch_permute");
+  DevGuard g(L->dev);
+  int64_t* tmp = nullptr;
+  if (cudaMalloc(&tmp, L->N * 8) != cudaSuccess) return fail(PP_ERR_OOM, "order staging allocation");
+  cudaError_t e = launch_order_to_nodes(L->d_order, L->d_node_set, L->N, tmp, L->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst_host, tmp, L->N * 8, cudaMemcpyDeviceToHost, L->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(L, e, "pp_get_order");
+  return PP_OK;
+}
+
+pp_status pp_read_store(pp_loader* L, int64_t row0, int64_t n, void* dst_host) {
+  if (!L || !dst_host) return fail(PP_ERR_INVALID, "NULL argument");
+  if (row0 < 0 || n < 0 || row0 + n > L->local_rows) return fail(PP_ERR_INVALID, "row range out of bounds");
+  DevGuard g(L->dev);
+  PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+  uint8_t* dst = static_cast<uint8_t*>(dst_host);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lr = row0 + i;
+    const uint8_t* src = lr < L->n_hbm ? L->d_store + lr * L->rec_stride : L->h_spill + (lr - L->n_hbm) * L->rec_stride;
+    PPL_CUDA(L, cudaMemcpy(dst + i * L->rec_in, src, L->rec_in, cudaMemcpyDefault));
+  }
+  return PP_OK;
+}
+
+pp_status pp_export_store(pp_loader* L, void* handle_out) {
+  if (!L || !handle_out) return fail(PP_ERR_INVALID, "NULL argument");
+  if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_export_store needs PP_PEERS_IPC");
+  DevGuard g(L->dev);
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_store));
+  memcpy(handle_out, &h, 64);
+  return PP_OK;
+}
+
+pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
+  if (!L || !handles) return fail(PP_ERR_INVALID, "NULL argument");
+  if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_import_peer_stores needs PP_PEERS_IPC");
+  if (L->linked) return fail(PP_ERR_STATE, "peers already imported");
+  DevGuard g(L->dev);
+  for (int o = 0; o < L->W; ++o) {
+    if (o == L->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * o, 64);
+    void* p = nullptr;
+    PPL_CUDA(L, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    L->ipc_opened.push_back(p);
+    const int64_t rows_o = (L->N_total - o + L->W - 1) / L->W;  // whole shard in HBM (checked at create)
+    L->shards[o] = ShardView{static_cast<const uint8_t*>(p), nullptr, rows_o};
+  }
+  L->linked = true;
+  return PP_OK;
+}
+
+pp_status pp_link_loopback(pp_loader* const* Ls, int32_t W) {
+  if (!Ls || W < 2 || W > kMaxWorld) return fail(PP_ERR_INVALID, "need 2..%d loaders", kMaxWorld);
+  for (int r = 0; r < W; ++r) {
+    const pp_loader* L = Ls[r];
+    if (!L) return fail(PP_ERR_INVALID, "loader %d is NULL", r);
+    if (L->desc.peers != PP_PEERS_LOOPBACK || L->W != W || L->rank != r)
+      return fail(PP_ERR_INVALID, "loader %d: not a loopback rank %d of %d", r, r, W);
+    if (L->dev != Ls[0]->dev || L->H != Ls[0]->H || L->F != Ls[0]->F || L->in_dtype != Ls[0]->in_dtype ||
+        L->N_total != Ls[0]->N_total || L->rec_stride != Ls[0]->rec_stride)
+      return fail(PP_ERR_INVALID, "loader %d: store shape differs from rank 0", r);
+  }
+  for (int r = 0; r < W; ++r) {
+    for (int o = 0; o < W; ++o) Ls[r]->shards[o] = ShardView{Ls[o]->d_store, Ls[o]->d_spill, Ls[o]->n_hbm};
+    Ls[r]->linked = true;
+  }
+  return PP_OK;
+}
+
+}  // extern "C"
