@@ -1,0 +1,81 @@
+"""The real multi-process sharded path (PP_PEERS_IPC) with two processes on ONE GPU:
+CUDA IPC handles are exchanged over gloo and each rank reads the other's store through
+the imported mapping -- the same code that reads a peer GPU's HBM over NVLink."""
+import os
+import socket
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, chunk, q):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2504_13266_b200 as pp
+    from inputs import hop_tensor
+    from paper_2504_13266_b200 import dist as ppd
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        H, N, F, B = 4, 6007, 64, 96
+        X, hs, rs = hop_tensor(40, H, N, F)
+        L = pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                      batch_size=B, out_dtype=pp.PP_BF16, world_size=world, rank=rank, peers=pp.PP_PEERS_IPC)
+        ppd.link_ipc(L)
+        ppd.check_epoch_args(17, chunk)
+        L.epoch_permute(17, chunk)
+        order = oracle.epoch_order(17, N, chunk)
+        out = torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda")
+        nodes = torch.empty(B, dtype=torch.int64, device="cuda")
+        t, bad = 0, 0
+        while (rows := L.next_batch(out, None, nodes)) >= 0:
+            torch.cuda.synchronize()
+            want, _, wn = oracle.batch(X.view(np.uint32), oracle.F32, hs, rs, H, F, order, B, world, t, rank,
+                                       oracle.BF16)
+            got = out[:rows].view(torch.int16).cpu().numpy().view(np.uint16)
+            bad += int(not np.array_equal(got, want)) + int(not np.array_equal(nodes[:rows].cpu().numpy(), wn))
+            t += 1
+        dist.barrier()  # peers keep their stores alive until everyone is done
+        L.close()
+        q.put((rank, bad, t == oracle.num_steps(N, B, world)))
+    except Exception as e:  # pragma: no cover - reported through the queue
+        q.put((rank, repr(e), False))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunk", [1, 64])
+def test_ipc_two_processes_one_gpu(chunk):
+    import torch.multiprocessing as mp
+
+    import __graft_entry__ as ge
+
+    ge.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, chunk, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, bad, steps_ok in res:
+        assert bad == 0 and steps_ok, (rank, bad)
