@@ -1,8 +1,11 @@
 """Benchmark of the PP-GNN mini-batch loading hot path (arXiv 2504.13266) on B200.
 
 A "step" is one epoch of the whole hot path: pp_epoch_permute
-(SGD-RR Philox argsort) + every batch of the epoch assembled with the fused
-fp32 -> bf16 cast (one pp_next_batch call per batch).  value = nodes/s.
+(SGD-RR Philox argsort; the next epoch's order is prefetched on a side stream so it
+overlaps this epoch's batches) + every batch of the epoch assembled with the fused
+fp32 -> bf16 cast, k batches per pp_next_batches launch (default k = 8, an 8-slot
+prefetch ring; k = 1 is one pp_next_batch call per batch, also reported).
+value = nodes/s.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--chunk c]
                   [--per-call k]  (k batches per pp_next_batches launch; 1 = pp_next_batch)
@@ -204,75 +207,93 @@ def run_ours(args):
     # output ring: one slot per step of the epoch (> L2: outputs really go to DRAM)
     ring = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
     slot_bytes = B * H * F * 2
-    k = max(1, args.per_call)
-
-    def epoch(e, ev_mid=None):
-        L.epoch_permute(SEED0 + e, chunk, stream)
-        if ev_mid is not None:
-            ev_mid.record(stream)
-        done = 0
-        while done < steps:
-            if k == 1:
-                L.next_batch(ring[done], None, None, stream)
-                done += 1
-            else:
-                done += len(L.next_batches(min(k, steps - done), ring[done], slot_bytes, None, None, stream))
-
     # rows this rank assembles per epoch (for the algorithmic bytes)
     my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
-    launches_per_epoch = (6 + (2 if chunk > 1 else 0)) + (steps if k == 1 else -(-steps // k))
+    U = -(-N // chunk)
+    # kernels of ours per permutation: one-CTA sort (U <= 4096) or the 6-kernel bucket sort
+    # (+ ragged-chunk search), + the chunk expansion when chunk > 1
+    perm_kernels = (1 if U <= 4096 else 6 + (chunk > 1)) + (chunk > 1)
 
-    with torch.cuda.stream(stream):
-        for e in range(args.warmup):
-            epoch(e)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    def timed(k, nsteps, sampler_index=None):
+        def epoch(e, ev_mid=None):
+            L.epoch_permute(SEED0 + e, chunk, stream)
+            if args.prefetch:
+                L.epoch_prefetch(SEED0 + e + 1, chunk)  # next epoch's order overlaps this epoch's batches
+            if ev_mid is not None:
+                ev_mid.record(stream)
+            done = 0
+            while done < steps:
+                if k == 1:
+                    L.next_batch(ring[done], None, None, stream)
+                    done += 1
+                else:
+                    done += len(L.next_batches(min(k, steps - done), ring[done], slot_bytes, None, None, stream))
+
+        with torch.cuda.stream(stream):
+            for e in range(args.warmup):
+                epoch(e)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(nsteps)]
+        clk = ClockSampler(sampler_index if sampler_index is not None else -1)
+        if sampler_index is not None:
+            clk.__enter__()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             start.record(stream)
-            for i in range(args.steps):
+            for i in range(nsteps):
                 evs[i][0].record(stream)
                 epoch(args.warmup + i, evs[i][1])
                 evs[i][2].record(stream)
             end.record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    total_ms = start.elapsed_time(end)
-    gather_ms = sum(b.elapsed_time(c) for _, b, c in evs)
-    perm_ms = sum(a.elapsed_time(b) for a, b, _ in evs)
-    if dist:
-        t = torch.tensor([total_ms, gather_ms, perm_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, gather_ms, perm_ms = t.tolist()
-    ms_per_step = total_ms / args.steps
-    value = N * args.steps / (total_ms / 1e3)  # all ranks together assemble N rows per epoch
+        if sampler_index is not None:
+            clk.__exit__(None, None, None)
+        if dist:
+            dist.barrier()
+        t = [start.elapsed_time(end), sum(b.elapsed_time(c) for _, b, c in evs),
+             sum(a.elapsed_time(b) for a, b, _ in evs)]
+        if dist:
+            tt = torch.tensor(t, device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = tt.tolist()
+        launches = -(-steps // k)
+        per_launch_ms = t[1] / (nsteps * launches)
+        bytes_per_launch = my_rows * (rec_in + rec_out + 4) / launches
+        return {"total_ms": t[0], "gather_ms": t[1], "perm_ms": t[2], "per_launch_ms": per_launch_ms,
+                "bytes_per_launch": bytes_per_launch, "achieved": bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
+                "launches": launches, "clocks": clk.summary() if sampler_index is not None else None}
 
+    k = max(1, args.per_call)
+    m = timed(k, args.steps, sampler_index=local)
+    ms_per_step = m["total_ms"] / args.steps
+    value = N * args.steps / (m["total_ms"] / 1e3)  # all ranks together assemble N rows per epoch
     peak, peak_kind = peaks()
-    gather_launches = steps if k == 1 else -(-steps // k)
-    per_launch_ms = gather_ms / (args.steps * gather_launches)
-    bytes_per_launch = my_rows * (rec_in + rec_out + 4) / gather_launches
-    achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+    roofline = {"bound": "hbm", "achieved": m["achieved"], "peak": peak, "unit": "GB/s", "frac": m["achieved"] / peak,
                 "traffic": committed_traffic(f"gather_{name}_k{k}"), "kernel": "k_gather_vec<bf16>",
-                "peak_kind": peak_kind, "per_launch_us": per_launch_ms * 1e3,
-                "algorithmic_bytes_per_launch": bytes_per_launch,
-                "frac_of_8TBs_nominal": achieved / 8000.0,
-                "permute_ms_per_epoch": perm_ms / args.steps}
+                "peak_kind": peak_kind, "per_launch_us": m["per_launch_ms"] * 1e3,
+                "algorithmic_bytes_per_launch": m["bytes_per_launch"],
+                "algorithmic_bytes_per_node": rec_in + rec_out + 4,
+                "frac_of_8TBs_nominal": m["achieved"] / 8000.0,
+                "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
+                        "(includes launch gaps and the overlapped next-epoch permutation)"}
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if W == 1 else "strong",
         "vs_baseline": None, "dtype": "f32->bf16", "data": "synthetic (§8(d) generator G, filled in place)",
         "config": config_dict(name, cfg, W, "inputs > L2 (3.9 GB store), outputs rotate over a "
-                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring"),
-        "roofline": roofline, "gpu_launches": launches_per_epoch * args.steps, "clocks": clk.summary(),
-        "batches_per_launch": k,
+                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring (one slot per step)"),
+        "roofline": roofline, "gpu_launches": (perm_kernels + m["launches"]) * args.steps, "clocks": m["clocks"],
+        "batches_per_launch": k, "prefetch_next_epoch_order": bool(args.prefetch),
     }
+    if k != 1 and not args.skip_k1:
+        m1 = timed(1, max(3, args.steps // 2))
+        result["per_batch_call"] = {
+            "value": N * max(3, args.steps // 2) / (m1["total_ms"] / 1e3), "unit": UNIT,
+            "ms_per_step": m1["total_ms"] / max(3, args.steps // 2), "achieved_GBs": m1["achieved"],
+            "note": "one pp_next_batch call (one launch) per batch from Python; host-bound (~5.6 us per ctypes call)"}
     del ring
     L.close()
     torch.cuda.empty_cache()
@@ -342,7 +363,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--chunk", type=int, default=None)
-    ap.add_argument("--per-call", type=int, default=1, help="batches per launch (pp_next_batches)")
+    ap.add_argument("--per-call", type=int, default=8,
+                    help="batches per pp_next_batches launch (an 8-slot prefetch ring); 1 = pp_next_batch")
+    ap.add_argument("--skip-k1", action="store_true", help="skip the secondary one-call-per-batch measurement")
+    ap.add_argument("--prefetch", type=int, default=1, help="overlap the next epoch's permutation (1/0)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()

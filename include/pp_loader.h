@@ -148,6 +148,15 @@ pp_status pp_loader_destroy(pp_loader* L);
  * Errors: PP_ERR_INVALID (chunk out of range), PP_ERR_CUDA. */
 pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream);
 
+/* Compute the order of a FUTURE epoch now, on a library side stream, so that
+ * it overlaps the current epoch's batches (the per-epoch shuffle runs "at the
+ * start of each epoch"; prefetching it is the double-buffer idea
+ * of PAPER.md:262 applied to the order).  The next pp_epoch_permute with the
+ * same (seed, chunk) only switches to the prefetched order; a permute with
+ * other arguments discards it.  At most one prefetch is pending (a second call
+ * replaces the first).  Errors: PP_ERR_INVALID (chunk), PP_ERR_CUDA. */
+pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk);
+
 /* Assemble this rank's batch of the current step into `out` and advance the
  * cursor.  out: device, [B][H][F] of out_dtype, contiguous, caller-owned,
  * 16-byte aligned for the vector path.  out_labels: device int32 [B] or NULL
@@ -158,6 +167,10 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
  * consumer_stream before this call, and is valid for work enqueued on
  * consumer_stream after it.  Alternating two buffers therefore overlaps the
  * assembly of batch t+1 with the consumer's work on batch t (double buffer).
+ * When consumer_stream is the loader stream (pp_set_stream), consecutive
+ * batches of one epoch may execute concurrently (programmatic dependent
+ * launch): give each call its own buffer, or put the consumer's kernels
+ * between two calls that reuse one.
  * Errors: PP_ERR_STATE (no permute yet), PP_END_OF_EPOCH (*rows = 0),
  * PP_ERR_INVALID, PP_ERR_CUDA. */
 pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* out_nodes,

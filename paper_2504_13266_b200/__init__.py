@@ -23,7 +23,7 @@ from ._abi import (  # noqa: F401
 
 __all__ = [
     "Loader", "PPError", "lib", "LIB_PATH",
-    "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_next_batch", "pp_next_batches",
+    "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_epoch_prefetch", "pp_next_batch", "pp_next_batches",
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
     "pp_import_peer_stores", "pp_debug_set_sort_bits_delta",
@@ -131,6 +131,10 @@ def pp_epoch_permute(h, seed: int, chunk: int = 1, stream=None) -> None:
     _check(lib().pp_epoch_permute(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk, _stream(stream)), "pp_epoch_permute")
 
 
+def pp_epoch_prefetch(h, seed: int, chunk: int = 1) -> None:
+    _check(lib().pp_epoch_prefetch(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk), "pp_epoch_prefetch")
+
+
 def pp_next_batch(h, out, out_labels=None, out_nodes=None, consumer_stream=None) -> int:
     """Returns the rows written, or -1 at the end of the epoch (PP_END_OF_EPOCH)."""
     rows = ctypes.c_int32()
@@ -228,6 +232,9 @@ class Loader:
 
     def epoch_permute(self, seed, chunk=1, stream=None):
         pp_epoch_permute(self.h, seed, chunk, stream)
+
+    def epoch_prefetch(self, seed, chunk=1):
+        pp_epoch_prefetch(self.h, seed, chunk)
 
     def next_batch(self, out, out_labels=None, out_nodes=None, consumer_stream=None):
         return pp_next_batch(self.h, out, out_labels, out_nodes, consumer_stream)

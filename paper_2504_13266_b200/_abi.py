@@ -15,7 +15,7 @@ PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK = 0, 1, 2
 
 # every symbol include/pp_loader.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_next_batch", "pp_next_batches", "pp_seek",
+    "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_epoch_prefetch", "pp_next_batch", "pp_next_batches", "pp_seek",
     "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
     "pp_read_store", "pp_debug_set_sort_bits_delta",
@@ -93,6 +93,7 @@ def lib():
                 "pp_loader_create": (st, [P, P]),
                 "pp_loader_destroy": (st, [P]),
                 "pp_epoch_permute": (st, [P, u64, i64, P]),
+                "pp_epoch_prefetch": (st, [P, u64, i64]),
                 "pp_next_batch": (st, [P, P, P, P, P, P]),
                 "pp_next_batches": (st, [P, i32, P, i64, P, P, P, P, P]),
                 "pp_seek": (st, [P, i64]),

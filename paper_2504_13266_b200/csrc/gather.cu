@@ -30,9 +30,10 @@
 
 namespace ppl {
 
-constexpr int kTileRows = 32;
+constexpr int kMaxTileRows = 32;
 constexpr int kGatherThreads = 256;
 constexpr int kUnroll = 4;
+constexpr int kMinBlocksPerSM = 4;  // caps registers at 64 -> 32 resident warps per SM
 
 enum { kF32 = 0, kBF16 = 1, kF16 = 2 };
 enum { kModeBF16 = 0, kModeF16 = 1, kModeCopy = 2 };
@@ -91,10 +92,14 @@ __device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, 
 // Vector path: MODE bf16/f16 reads 32 B (8 fp32) and writes 16 B; copy mode
 // moves 16 B.  vpr = vector slots per row.
 template <int MODE, bool SHARDED>
-__global__ void __launch_bounds__(kGatherThreads) k_gather_vec(const GatherArgs a, uint32_t vpr, uint64_t vpr_M,
-                                                               int64_t row_out_bytes) {
-  __shared__ const uint8_t* s_src[2][kTileRows];
+__global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
+    k_gather_vec(const GatherArgs a, uint32_t vpr, uint64_t vpr_M, int64_t row_out_bytes) {
+  __shared__ const uint8_t* s_src[2][kMaxTileRows];
+  // Programmatic dependent launch: the next batch's gather may start as soon as
+  // every CTA of this one is running (batches are independent; see launch_gather).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kInBytes = (MODE == kModeCopy) ? 16 : 32;
+  const int kTileRows = a.tile_rows;
   const int64_t tiles_per_step = (a.B + kTileRows - 1) / kTileRows;
   const int64_t total_tiles = tiles_per_step * a.nsteps;
   int buf = 0;
@@ -150,8 +155,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_vec(const GatherArgs 
 // Scalar fallback for records whose size / alignment rule out the vector
 // path.  Same tile structure, one element per slot.
 template <bool SHARDED>
-__global__ void __launch_bounds__(kGatherThreads) k_gather_scalar(const GatherArgs a, uint32_t HF, uint64_t HF_M) {
-  __shared__ const uint8_t* s_src[2][kTileRows];
+__global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
+    k_gather_scalar(const GatherArgs a, uint32_t HF, uint64_t HF_M) {
+  __shared__ const uint8_t* s_src[2][kMaxTileRows];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int kTileRows = a.tile_rows;
   const int s_in = a.in_dtype == kF32 ? 4 : 2;
   const int s_out = a.out_dtype == kF32 ? 4 : 2;
   const int64_t row_out_bytes = static_cast<int64_t>(HF) * s_out;
@@ -202,10 +210,27 @@ bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t r
   return in_row % 32 == 0;  // fp32 -> 16-bit: 8 elements per slot
 }
 
-cudaError_t launch_gather(const GatherArgs& a, bool vector_path, cudaStream_t st) {
-  const int64_t tiles = ((a.B + kTileRows - 1) / kTileRows) * static_cast<int64_t>(a.nsteps);
+template <typename Kern, typename... Args>
+static cudaError_t launch_ex(Kern kern, uint32_t grid, bool pdl, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGatherThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int grid_per_sm, cudaStream_t st) {
+  if (a.tile_rows < 1 || a.tile_rows > kMaxTileRows) return cudaErrorInvalidValue;
+  const int64_t tiles = ((a.B + a.tile_rows - 1) / a.tile_rows) * static_cast<int64_t>(a.nsteps);
   if (tiles <= 0) return cudaSuccess;
-  const int64_t grid = tiles < 148 * 8 ? tiles : 148 * 8;  // 8 resident 256-thread CTAs per SM
+  const int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  const uint32_t grid = static_cast<uint32_t>(tiles < cap ? tiles : cap);
   const bool sharded = a.W > 1;
   const int s_out = a.out_dtype == kF32 ? 4 : 2;
   if (vector_path) {
@@ -213,22 +238,18 @@ cudaError_t launch_gather(const GatherArgs& a, bool vector_path, cudaStream_t st
     const int64_t row_out_bytes = static_cast<int64_t>(a.HF) * s_out;
     const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
     const uint64_t M = ((1ull << 40) + vpr - 1) / vpr;
-    if (static_cast<uint64_t>(kTileRows) * vpr * vpr >= (1ull << 40)) return cudaErrorInvalidValue;
-#define PPL_GV(MODE, SH) k_gather_vec<MODE, SH><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, vpr, M, row_out_bytes)
+    if (static_cast<uint64_t>(kMaxTileRows) * vpr * vpr >= (1ull << 40)) return cudaErrorInvalidValue;
+#define PPL_GV(MODE, SH) return launch_ex(k_gather_vec<MODE, SH>, grid, pdl, st, a, vpr, M, row_out_bytes)
     if (mode == kModeBF16) { if (sharded) PPL_GV(kModeBF16, true); else PPL_GV(kModeBF16, false); }
     else if (mode == kModeF16) { if (sharded) PPL_GV(kModeF16, true); else PPL_GV(kModeF16, false); }
     else { if (sharded) PPL_GV(kModeCopy, true); else PPL_GV(kModeCopy, false); }
 #undef PPL_GV
-  } else {
-    const uint32_t HF = static_cast<uint32_t>(a.HF);
-    if (static_cast<uint64_t>(kTileRows) * HF * HF >= (1ull << 40)) return cudaErrorInvalidValue;
-    const uint64_t M = ((1ull << 40) + HF - 1) / HF;
-    if (sharded)
-      k_gather_scalar<true><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, HF, M);
-    else
-      k_gather_scalar<false><<<static_cast<uint32_t>(grid), kGatherThreads, 0, st>>>(a, HF, M);
   }
-  return cudaGetLastError();
+  const uint32_t HF = static_cast<uint32_t>(a.HF);
+  if (static_cast<uint64_t>(kMaxTileRows) * HF * HF >= (1ull << 40)) return cudaErrorInvalidValue;
+  const uint64_t M = ((1ull << 40) + HF - 1) / HF;
+  if (sharded) return launch_ex(k_gather_scalar<true>, grid, pdl, st, a, HF, M);
+  return launch_ex(k_gather_scalar<false>, grid, pdl, st, a, HF, M);
 }
 
 // ---- K10: synthetic fill (SURVEY.md §8(d) generators G / G16) ----------------

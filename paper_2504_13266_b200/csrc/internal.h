@@ -31,12 +31,14 @@ constexpr int kScanTile = 4096;
 // Buckets used for U units: 2^bits with U / 2^bits in ~[14, 28).
 int sort_bucket_bits(uint64_t U, int delta);
 
-// pi[0..U) = units sorted by (Philox key, unit id).  All on `st`.
-cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, const SortScratch& s, uint32_t* pi,
-                                    cudaStream_t st);
+// pi[0..U) = units sorted by (Philox key, unit id); if ragged != null also
+// *ragged = position of unit U-1 in pi.  U <= 4096 (and bits >= 0): one-CTA
+// bitonic sort; otherwise the bucket sort.  All on `st`.
+cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool allow_cta, const SortScratch& s, uint32_t* pi,
+                                    uint32_t* ragged, cudaStream_t st);
 
 // order[p], p in [0, N): chunk expansion of pi (chunk c, U = ceil(N / c)).
-cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, uint32_t* ragged,
+cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, const uint32_t* ragged,
                                 uint32_t* order, cudaStream_t st);
 
 // ---- batch assembly (gather.cu) ----------------------------------------------
@@ -58,11 +60,15 @@ struct GatherArgs {
   int64_t rec_stride;       // store pitch (bytes)
   int32_t HF;               // elements per record
   int32_t in_dtype, out_dtype;  // pp_dtype codes
+  int32_t tile_rows;        // batch rows per CTA tile (1..32)
+  int32_t num_sms;
 };
 
-// Returns cudaErrorInvalidValue when the vector path's alignment rules are
-// not met and `allow_scalar` is false.
-cudaError_t launch_gather(const GatherArgs& a, bool vector_path, cudaStream_t st);
+// One launch assembling a.nsteps steps.  pdl: launch with programmatic stream
+// serialization (may overlap the previous gather on the stream; only valid
+// when the previous kernel on `st` is a gather of the same epoch).
+// grid_per_sm caps the persistent grid at num_sms * grid_per_sm CTAs.
+cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int grid_per_sm, cudaStream_t st);
 bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride);
 
 // ---- synthetic fill (gather.cu) ---------------------------------------------

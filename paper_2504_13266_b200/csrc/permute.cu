@@ -188,9 +188,63 @@ __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32
   }
 }
 
-cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, const SortScratch& s, uint32_t* pi,
-                                    cudaStream_t st) {
+// K2: small unit counts (chunk reshuffling: U = ceil(N / c), e.g. 299 chunks of
+// 8192 products rows) -- one CTA computes every key into shared memory and
+// bitonic-sorts the (key, id) pairs; padding sorts last.  Also records where
+// the ragged chunk U-1 landed (needed by the chunk expansion).
+constexpr uint32_t kCtaSortMax = 4096;
+constexpr int kCtaSortThreads = 1024;
+
+__global__ void __launch_bounds__(kCtaSortThreads) k_cta_sort(uint64_t seed, uint32_t U, uint32_t P,
+                                                              uint32_t* __restrict__ pi,
+                                                              uint32_t* __restrict__ ragged) {
+  extern __shared__ uint64_t smem_keys[];
+  uint32_t* ids = reinterpret_cast<uint32_t*>(smem_keys + P);
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+    smem_keys[i] = i < U ? unit_sort_key(seed, i) : ~0ull;
+    ids[i] = i < U ? i : 0xffffffffu;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t ka = smem_keys[i], kb = smem_keys[l];
+          const uint32_t ia = ids[i], ib = ids[l];
+          const bool a_gt_b = (ka > kb) || (ka == kb && ia > ib);
+          if (a_gt_b == ((i & k) == 0)) {
+            smem_keys[i] = kb;
+            smem_keys[l] = ka;
+            ids[i] = ib;
+            ids[l] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < U; i += blockDim.x) {
+    pi[i] = ids[i];
+    if (ragged != nullptr && ids[i] == U - 1) *ragged = i;
+  }
+}
+
+// Position of the ragged (last) chunk U-1 inside pi.
+__global__ void k_find_ragged(const uint32_t* __restrict__ pi, uint32_t U, uint32_t* __restrict__ ragged) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x)
+    if (pi[i] == U - 1) *ragged = i;
+}
+
+cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool allow_cta, const SortScratch& s, uint32_t* pi,
+                                    uint32_t* ragged, cudaStream_t st) {
   if (U == 0) return cudaSuccess;
+  if (U <= kCtaSortMax && allow_cta) {
+    uint32_t P = 1;
+    while (P < U) P <<= 1;
+    k_cta_sort<<<1, kCtaSortThreads, P * 12, st>>>(seed, U, P, pi, ragged);
+    return cudaGetLastError();
+  }
   const uint32_t nb = 1u << bits;
   const uint32_t n = nb + 1;  // counts[nb] = 0 -> offsets[nb] = U
   cudaError_t e = cudaMemsetAsync(s.counts, 0, sizeof(uint32_t) * n, st);
@@ -205,13 +259,8 @@ cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, const S
   k_scatter<<<unit_blocks, threads, 0, st>>>(seed, U, bits, s.cursor, s.tmp);
   const uint64_t rank_threads = static_cast<uint64_t>(nb) * 32;
   k_bucket_rank<<<static_cast<uint32_t>((rank_threads + 255) / 256), 256, 0, st>>>(seed, s.counts, nb, s.tmp, pi);
+  if (ragged != nullptr) k_find_ragged<<<std::min<uint32_t>((U + 255) / 256, 148u * 8u), 256, 0, st>>>(pi, U, ragged);
   return cudaGetLastError();
-}
-
-// Position of the ragged (last) chunk U-1 inside pi.
-__global__ void k_find_ragged(const uint32_t* __restrict__ pi, uint32_t U, uint32_t* __restrict__ ragged) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x)
-    if (pi[i] == U - 1) *ragged = i;
 }
 
 // order = concat over i of [pi_i * c, min(pi_i * c + c, N)) (oracle step O7).
@@ -219,6 +268,7 @@ __global__ void k_find_ragged(const uint32_t* __restrict__ pi, uint32_t U, uint3
 // sits at r*c, chunks after it start at i*c - (c - ls).
 __global__ void k_chunk_expand(const uint32_t* __restrict__ pi, uint64_t N, uint64_t c, uint64_t ls,
                                const uint32_t* __restrict__ ragged, uint32_t* __restrict__ order) {
+  // ragged = position of chunk U-1 in pi (written by the permutation launch)
   const uint64_t r = *ragged;
   const uint64_t rag_begin = r * c;
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < N;
@@ -240,11 +290,10 @@ __global__ void k_chunk_expand(const uint32_t* __restrict__ pi, uint64_t N, uint
   }
 }
 
-cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, uint32_t* ragged,
+cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, const uint32_t* ragged,
                                 uint32_t* order, cudaStream_t st) {
   if (N == 0) return cudaSuccess;
   const uint64_t ls = N - static_cast<uint64_t>(U - 1) * c;
-  k_find_ragged<<<std::min<uint32_t>((U + 255) / 256, 148u * 8u), 256, 0, st>>>(pi, U, ragged);
   const uint64_t blocks = std::min<uint64_t>((N + 255) / 256, 148ull * 16ull);
   k_chunk_expand<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(pi, N, c, ls, ragged, order);
   return cudaGetLastError();

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -68,7 +69,9 @@ struct pp_loader {
   int32_t* d_labels = nullptr;
   bool has_labels = false;
 
-  uint32_t* d_order = nullptr;
+  uint32_t* d_orders[2] = {nullptr, nullptr};  // current epoch + prefetched next epoch
+  int cur = 0;
+  uint32_t* d_order = nullptr;                  // == d_orders[cur]
   uint32_t* d_pi = nullptr;
   int64_t pi_cap = 0;
   SortScratch sort{};
@@ -78,6 +81,18 @@ struct pp_loader {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t pstream = nullptr;  // side stream for pp_epoch_prefetch
+  cudaEvent_t ev_pref = nullptr, ev_pref_in = nullptr;
+  bool pref_pending = false;
+  uint64_t pref_seed = 0;
+  int64_t pref_chunk = 0;
+
+  // launch tuning (defaults; PPLOAD_TILE_ROWS / PPLOAD_PDL / PPLOAD_GRID_PER_SM override)
+  int num_sms = 148;
+  int tile_rows = 16;
+  bool pdl = true;
+  int grid_per_sm = 4;
+  bool last_was_gather = false;  // previous op on the loader stream is a gather of this epoch
 
   ShardView shards[kMaxWorld]{};
   bool linked = false;
@@ -109,7 +124,9 @@ void release(pp_loader* L) {
   if (L->h_spill) cudaFreeHost(L->h_spill);
   cudaFree(L->d_node_set);
   cudaFree(L->d_labels);
-  cudaFree(L->d_order);
+  if (L->pstream) cudaStreamSynchronize(L->pstream);
+  cudaFree(L->d_orders[0]);
+  cudaFree(L->d_orders[1]);
   cudaFree(L->d_pi);
   cudaFree(L->sort.counts);
   cudaFree(L->sort.cursor);
@@ -118,6 +135,9 @@ void release(pp_loader* L) {
   cudaFree(L->sort.ragged);
   if (L->ev_in) cudaEventDestroy(L->ev_in);
   if (L->ev_out) cudaEventDestroy(L->ev_out);
+  if (L->ev_pref) cudaEventDestroy(L->ev_pref);
+  if (L->ev_pref_in) cudaEventDestroy(L->ev_pref_in);
+  if (L->pstream) cudaStreamDestroy(L->pstream);
   if (L->own_stream && L->stream) cudaStreamDestroy(L->stream);
   delete L;
 }
@@ -291,17 +311,25 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (cudaMemcpy(L->d_labels, desc->labels, L->N_total * 4, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "labels upload"));
   }
-  if (cudaMalloc(&L->d_order, L->N * 4) != cudaSuccess || cudaMalloc(&L->sort.tmp, L->N * 4) != cudaSuccess ||
-      cudaMalloc(&L->sort.ragged, 4) != cudaSuccess)
+  if (cudaMalloc(&L->d_orders[0], L->N * 4) != cudaSuccess || cudaMalloc(&L->d_orders[1], L->N * 4) != cudaSuccess ||
+      cudaMalloc(&L->sort.tmp, L->N * 4) != cudaSuccess || cudaMalloc(&L->sort.ragged, 4) != cudaSuccess)
     return bail(fail(PP_ERR_OOM, "order / sort scratch allocation"));
+  L->d_order = L->d_orders[0];
   st = ensure_sort_scratch(L, static_cast<uint32_t>(L->N), sort_bucket_bits(L->N, 0));
   if (st != PP_OK) return bail(st);
   if (cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(PP_ERR_CUDA, "stream creation"));
   L->own_stream = true;
   if (cudaEventCreateWithFlags(&L->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&L->ev_out, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&L->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_pref, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_pref_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&L->pstream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(PP_ERR_CUDA, "event creation"));
+  cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, L->dev);
+  if (const char* e = getenv("PPLOAD_TILE_ROWS")) L->tile_rows = std::max(1, std::min(32, atoi(e)));
+  if (const char* e = getenv("PPLOAD_PDL")) L->pdl = atoi(e) != 0;
+  if (const char* e = getenv("PPLOAD_GRID_PER_SM")) L->grid_per_sm = std::max(1, atoi(e));
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
   L->linked = (L->W == 1);
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PP_ERR_CUDA, "create sync"));
@@ -324,12 +352,34 @@ pp_status pp_set_stream(pp_loader* L, void* stream) {
   if (L->own_stream) cudaStreamDestroy(L->stream);
   L->stream = static_cast<cudaStream_t>(stream);
   L->own_stream = false;
+  L->last_was_gather = false;
   return PP_OK;
 }
 
 pp_status pp_debug_set_sort_bits_delta(pp_loader* L, int32_t delta) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   L->sort_bits_delta = delta;
+  return PP_OK;
+}
+
+static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint32_t* order, cudaStream_t st) {
+  const uint32_t U = static_cast<uint32_t>((L->N + chunk - 1) / chunk);
+  const int bits = sort_bucket_bits(U, L->sort_bits_delta);
+  pp_status ps = ensure_sort_scratch(L, U, bits);
+  if (ps != PP_OK) return ps;
+  if (chunk == 1) {
+    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort_bits_delta == 0, L->sort, order, nullptr, st));
+  } else {
+    if (L->pi_cap < U) {
+      cudaFree(L->d_pi);
+      L->d_pi = nullptr;
+      if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
+      L->pi_cap = U;
+    }
+    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort_bits_delta == 0, L->sort, L->d_pi, L->sort.ragged, st));
+    PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(L->N), static_cast<uint64_t>(chunk),
+                                    L->sort.ragged, order, st));
+  }
   return PP_OK;
 }
 
@@ -343,31 +393,49 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
     PPL_CUDA(L, cudaEventRecord(L->ev_in, user));
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
   }
-  const uint32_t U = static_cast<uint32_t>((L->N + chunk - 1) / chunk);
-  const int bits = sort_bucket_bits(U, L->sort_bits_delta);
-  pp_status st = ensure_sort_scratch(L, U, bits);
-  if (st != PP_OK) return st;
-  if (chunk == 1) {
-    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort, L->d_order, L->stream));
-  } else {
-    if (L->pi_cap < U) {
-      cudaFree(L->d_pi);
-      L->d_pi = nullptr;
-      if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
-      L->pi_cap = U;
+  if (L->pref_pending) {
+    // the prefetch shares the sort scratch: order after it either way
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_pref, 0));
+    L->pref_pending = false;
+    if (L->pref_seed == seed && L->pref_chunk == chunk) {
+      L->cur ^= 1;  // the prefetched order becomes current
+      L->d_order = L->d_orders[L->cur];
+    } else {
+      pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream);
+      if (ps != PP_OK) return ps;
     }
-    PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort, L->d_pi, L->stream));
-    PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(L->N), static_cast<uint64_t>(chunk),
-                                    L->sort.ragged, L->d_order, L->stream));
+  } else {
+    pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream);
+    if (ps != PP_OK) return ps;
   }
   if (user != L->stream) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
   }
+  L->last_was_gather = false;
   L->permuted = true;
   L->seed = seed;
   L->chunk = chunk;
   L->cursor = 0;
+  return PP_OK;
+}
+
+pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
+  DevGuard g(L->dev);
+  if (L->pref_pending) PPL_CUDA(L, cudaStreamWaitEvent(L->pstream, L->ev_pref, 0));
+  // WAR on the spare order buffer (read by the previous epoch's batches) and on
+  // the sort scratch (used by work already enqueued on the loader stream)
+  PPL_CUDA(L, cudaEventRecord(L->ev_pref_in, L->stream));
+  PPL_CUDA(L, cudaStreamWaitEvent(L->pstream, L->ev_pref_in, 0));
+  pp_status ps = enqueue_order(L, seed, chunk, L->d_orders[L->cur ^ 1], L->pstream);
+  if (ps != PP_OK) return ps;
+  PPL_CUDA(L, cudaEventRecord(L->ev_pref, L->pstream));
+  L->pref_pending = true;
+  L->pref_seed = seed;
+  L->pref_chunk = chunk;
   return PP_OK;
 }
 
@@ -396,6 +464,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+    L->last_was_gather = false;
   }
   GatherArgs a{};
   a.order = L->d_order;
@@ -416,7 +485,13 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   a.HF = L->HF;
   a.in_dtype = L->in_dtype;
   a.out_dtype = L->out_dtype;
-  PPL_CUDA(L, launch_gather(a, vec, L->stream));
+  a.tile_rows = L->tile_rows;
+  a.num_sms = L->num_sms;
+  // Programmatic dependent launch only right after another gather of this epoch:
+  // batches of one epoch are independent, and the first gather after a permute
+  // or an event wait is fully serialised, so every gather sees a complete order.
+  PPL_CUDA(L, launch_gather(a, vec, L->pdl && L->last_was_gather, L->grid_per_sm, L->stream));
+  L->last_was_gather = !handoff;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));

@@ -415,3 +415,28 @@ def test_drop_last(pp):
         L.epoch_permute(1, 1)
         got = run_epoch(L, B, 1, 8, oracle.BF16)
         assert [g[0].shape[0] for g in got] == [B] * 10
+
+
+def test_epoch_prefetch(pp, tiny):
+    # the next epoch's order computed ahead on the side stream == computing it at permute time
+    hops, bits = tiny
+    H, N, F = hops.shape
+    B = 256
+    with pp.Loader(data=hops, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F,
+                   dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(1, 1)
+        L.epoch_prefetch(2, 1)
+        first = run_epoch(L, B, H, F, oracle.BF16)  # epoch 1 unaffected by the pending prefetch
+        check_epoch(first, bits, oracle.F32, N * F, F, H, F, oracle.epoch_order(1, N, 1), B, oracle.BF16)
+        L.epoch_permute(2, 1)  # matches: switch to the prefetched order
+        assert np.array_equal(L.get_order(), oracle.epoch_order(2, N, 1))
+        L.epoch_prefetch(3, 64)
+        L.epoch_permute(4, 16)  # does not match: computed afresh
+        assert np.array_equal(L.get_order(), oracle.epoch_order(4, N, 16))
+        got = run_epoch(L, B, H, F, oracle.BF16)
+        check_epoch(got, bits, oracle.F32, N * F, F, H, F, oracle.epoch_order(4, N, 16), B, oracle.BF16)
+        for e in range(5, 9):  # steady-state pipelining across epochs
+            L.epoch_prefetch(e, 7)
+            run_epoch(L, B, H, F, oracle.BF16)
+            L.epoch_permute(e, 7)
+            assert np.array_equal(L.get_order(), oracle.epoch_order(e, N, 7))
