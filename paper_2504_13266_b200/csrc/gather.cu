@@ -201,6 +201,146 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
   }
 }
 
+// ---- K4: bulk-copy (TMA engine) variant --------------------------------------
+// Whole node records are moved global -> shared by cp.async.bulk (one bulk copy
+// per batch row, issued by the lane that resolved the row), tracked by an
+// mbarrier per stage; all warps then convert shared -> registers -> 128-bit
+// global stores.  kStages tiles of rows are in flight per CTA, so the number
+// of outstanding bytes no longer depends on registers and the copy engine
+// issues large requests (this is the path for pinned-host (PCIe) and peer
+// (NVLink) sources, where request size and depth matter most).
+constexpr int kTmaStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int MODE, bool SHARDED>
+__global__ void __launch_bounds__(kGatherThreads, 2)
+    k_gather_tma(const GatherArgs a, uint32_t vpr, uint64_t vpr_M, int64_t row_out_bytes, int32_t rec_in,
+                 int32_t tr) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kTmaStages];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int kInBytes = (MODE == kModeCopy) ? 16 : 32;
+  const int64_t tiles_per_step = (a.B + tr - 1) / tr;
+  const int64_t total_tiles = tiles_per_step * a.nsteps;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // tile k of this CTA -> (step, first row, rows); rows <= 0 marks an empty tile
+  auto tile_of = [&](int64_t k, int64_t& step, int& j0, int64_t& step_pos) -> int {
+    const int64_t tile = blockIdx.x + k * gridDim.x;
+    if (tile >= total_tiles) return -1;
+    step = tile / tiles_per_step;
+    j0 = static_cast<int>(tile - step * tiles_per_step) * tr;
+    step_pos = a.first_pos + step * a.step_stride;
+    const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
+    return static_cast<int>(min(static_cast<int64_t>(tr), nrows_step - j0));
+  };
+  const int64_t stage_bytes = static_cast<int64_t>(tr) * rec_in;
+  // warp 0: resolve the rows of tile k and start their bulk copies into stage s
+  auto issue = [&](int64_t k) {
+    int64_t step, step_pos;
+    int j0;
+    const int rows = tile_of(k, step, j0, step_pos);
+    if (rows <= 0) return;
+    const int s = static_cast<int>(k % kTmaStages);
+    uint8_t* stage = smem + s * stage_bytes;
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * rec_in);
+    __syncwarp();
+    for (int j = lane; j < rows; j += 32) {
+      const int64_t p = step_pos + j0 + j;
+      uint64_t v = a.order[p];
+      if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
+      int owner = 0;
+      uint64_t lr = v;
+      if (SHARDED) {
+        owner = static_cast<int>(v % static_cast<uint64_t>(a.W));
+        lr = v / static_cast<uint64_t>(a.W);
+      }
+      const ShardView sh = a.shards[owner];
+      const int64_t l = static_cast<int64_t>(lr);
+      const uint8_t* src = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
+      bulk_g2s(stage + static_cast<int64_t>(j) * rec_in, src, static_cast<uint32_t>(rec_in), &full[s]);
+      const int64_t oj = step * a.B + j0 + j;
+      if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
+      if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
+    }
+  };
+  if (warp == 0)
+    for (int k = 0; k < kTmaStages; ++k) issue(k);
+  uint32_t phase = 0;  // bit s = parity of stage s
+  for (int64_t k = 0;; ++k) {
+    int64_t step, step_pos;
+    int j0;
+    const int rows = tile_of(k, step, j0, step_pos);
+    if (rows == -1) break;
+    const int s = static_cast<int>(k % kTmaStages);
+    if (rows > 0) {
+      mbar_wait(&full[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const uint8_t* stage = smem + s * stage_bytes;
+      uint8_t* out_tile = a.out + step * a.out_stride + static_cast<int64_t>(j0) * row_out_bytes;
+      const uint32_t nvec = static_cast<uint32_t>(rows) * vpr;
+      for (uint32_t e = threadIdx.x; e < nvec; e += kGatherThreads) {
+        const uint32_t r = fast_div(e, vpr_M);
+        const uint32_t c = e - r * vpr;
+        const uint4* src = reinterpret_cast<const uint4*>(stage + static_cast<int64_t>(r) * rec_in + c * kInBytes);
+        uint4 y;
+        if (MODE == kModeBF16) {
+          const uint4 x0 = src[0], x1 = src[1];
+          y = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
+        } else if (MODE == kModeF16) {
+          const uint4 x0 = src[0], x1 = src[1];
+          y = make_uint4(pack_f16(x0.x, x0.y), pack_f16(x0.z, x0.w), pack_f16(x1.x, x1.y), pack_f16(x1.z, x1.w));
+        } else {
+          y = src[0];
+        }
+        st_vec(out_tile + static_cast<int64_t>(r) * row_out_bytes + static_cast<int64_t>(c) * 16, y);
+      }
+    }
+    __syncthreads();  // every warp is done reading stage s
+    if (warp == 0) issue(k + kTmaStages);
+  }
+}
+
+// rows per stage for the bulk-copy path (0: record too large for it)
+static int tma_rows_per_stage(int64_t rec_in) {
+  if (rec_in % 16 != 0 || rec_in * kTmaStages > 96 * 1024) return 0;
+  int64_t tr = (24 * 1024) / rec_in;
+  if (tr < 1) tr = 1;
+  if (tr > 16) tr = 16;
+  return static_cast<int>(tr);
+}
+
 bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride) {
   const int s_in = in_dtype == kF32 ? 4 : 2;
   const int s_out = out_dtype == kF32 ? 4 : 2;
@@ -211,11 +351,11 @@ bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t r
 }
 
 template <typename Kern, typename... Args>
-static cudaError_t launch_ex(Kern kern, uint32_t grid, bool pdl, cudaStream_t st, Args... args) {
+static cudaError_t launch_ex(Kern kern, uint32_t grid, bool pdl, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGatherThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -225,7 +365,31 @@ static cudaError_t launch_ex(Kern kern, uint32_t grid, bool pdl, cudaStream_t st
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int grid_per_sm, cudaStream_t st) {
+bool gather_tma_ok(int32_t HF, int32_t in_dtype) {
+  return tma_rows_per_stage(static_cast<int64_t>(HF) * (in_dtype == kF32 ? 4 : 2)) > 0;
+}
+
+template <int MODE, bool SH>
+static cudaError_t launch_tma(const GatherArgs& a, bool pdl, int grid_per_sm, cudaStream_t st, uint32_t vpr,
+                              uint64_t M, int64_t row_out_bytes) {
+  const int32_t rec_in = a.HF * (a.in_dtype == kF32 ? 4 : 2);
+  const int tr = tma_rows_per_stage(rec_in);
+  if (tr == 0) return cudaErrorInvalidValue;
+  const size_t smem = static_cast<size_t>(kTmaStages) * tr * rec_in;
+  static bool attr_set = false;  // per (MODE, SH) instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gather_tma<MODE, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         96 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t tiles = ((a.B + tr - 1) / tr) * static_cast<int64_t>(a.nsteps);
+  const int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  const uint32_t grid = static_cast<uint32_t>(tiles < cap ? tiles : cap);
+  return launch_ex(k_gather_tma<MODE, SH>, grid, pdl, smem, st, a, vpr, M, row_out_bytes, rec_in, tr);
+}
+
+cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_sm, cudaStream_t st) {
   if (a.tile_rows < 1 || a.tile_rows > kMaxTileRows) return cudaErrorInvalidValue;
   const int64_t tiles = ((a.B + a.tile_rows - 1) / a.tile_rows) * static_cast<int64_t>(a.nsteps);
   if (tiles <= 0) return cudaSuccess;
@@ -233,13 +397,24 @@ cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int g
   const uint32_t grid = static_cast<uint32_t>(tiles < cap ? tiles : cap);
   const bool sharded = a.W > 1;
   const int s_out = a.out_dtype == kF32 ? 4 : 2;
-  if (vector_path) {
+  if (path == kPathTma) {
+    const int mode = (a.in_dtype == a.out_dtype) ? kModeCopy : (a.out_dtype == kBF16 ? kModeBF16 : kModeF16);
+    const int64_t row_out_bytes = static_cast<int64_t>(a.HF) * s_out;
+    const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
+    const uint64_t M = ((1ull << 40) + vpr - 1) / vpr;
+#define PPL_GT(MODE, SH) return launch_tma<MODE, SH>(a, pdl, 2, st, vpr, M, row_out_bytes)
+    if (mode == kModeBF16) { if (sharded) PPL_GT(kModeBF16, true); else PPL_GT(kModeBF16, false); }
+    else if (mode == kModeF16) { if (sharded) PPL_GT(kModeF16, true); else PPL_GT(kModeF16, false); }
+    else { if (sharded) PPL_GT(kModeCopy, true); else PPL_GT(kModeCopy, false); }
+#undef PPL_GT
+  }
+  if (path == kPathVector) {
     const int mode = (a.in_dtype == a.out_dtype) ? kModeCopy : (a.out_dtype == kBF16 ? kModeBF16 : kModeF16);
     const int64_t row_out_bytes = static_cast<int64_t>(a.HF) * s_out;
     const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
     const uint64_t M = ((1ull << 40) + vpr - 1) / vpr;
     if (static_cast<uint64_t>(kMaxTileRows) * vpr * vpr >= (1ull << 40)) return cudaErrorInvalidValue;
-#define PPL_GV(MODE, SH) return launch_ex(k_gather_vec<MODE, SH>, grid, pdl, st, a, vpr, M, row_out_bytes)
+#define PPL_GV(MODE, SH) return launch_ex(k_gather_vec<MODE, SH>, grid, pdl, 0, st, a, vpr, M, row_out_bytes)
     if (mode == kModeBF16) { if (sharded) PPL_GV(kModeBF16, true); else PPL_GV(kModeBF16, false); }
     else if (mode == kModeF16) { if (sharded) PPL_GV(kModeF16, true); else PPL_GV(kModeF16, false); }
     else { if (sharded) PPL_GV(kModeCopy, true); else PPL_GV(kModeCopy, false); }
@@ -248,8 +423,8 @@ cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int g
   const uint32_t HF = static_cast<uint32_t>(a.HF);
   if (static_cast<uint64_t>(kMaxTileRows) * HF * HF >= (1ull << 40)) return cudaErrorInvalidValue;
   const uint64_t M = ((1ull << 40) + HF - 1) / HF;
-  if (sharded) return launch_ex(k_gather_scalar<true>, grid, pdl, st, a, HF, M);
-  return launch_ex(k_gather_scalar<false>, grid, pdl, st, a, HF, M);
+  if (sharded) return launch_ex(k_gather_scalar<true>, grid, pdl, 0, st, a, HF, M);
+  return launch_ex(k_gather_scalar<false>, grid, pdl, 0, st, a, HF, M);
 }
 
 // ---- K10: synthetic fill (SURVEY.md §8(d) generators G / G16) ----------------

@@ -68,8 +68,10 @@ struct GatherArgs {
 // serialization (may overlap the previous gather on the stream; only valid
 // when the previous kernel on `st` is a gather of the same epoch).
 // grid_per_sm caps the persistent grid at num_sms * grid_per_sm CTAs.
-cudaError_t launch_gather(const GatherArgs& a, bool vector_path, bool pdl, int grid_per_sm, cudaStream_t st);
+enum { kPathVector = 0, kPathScalar = 1, kPathTma = 2 };
+cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_sm, cudaStream_t st);
 bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride);
+bool gather_tma_ok(int32_t HF, int32_t in_dtype);  // record fits the bulk-copy stages
 
 // ---- synthetic fill (gather.cu) ---------------------------------------------
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,

@@ -92,6 +92,8 @@ struct pp_loader {
   int tile_rows = 16;
   bool pdl = true;
   int grid_per_sm = 4;
+  int gather_mode = 0;           // 0 auto, 1 ldg (register-staged), 2 tma (bulk copy); PPLOAD_GATHER
+  bool tma_ok = false;
   bool last_was_gather = false;  // previous op on the loader stream is a gather of this epoch
 
   ShardView shards[kMaxWorld]{};
@@ -330,6 +332,8 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   if (const char* e = getenv("PPLOAD_TILE_ROWS")) L->tile_rows = std::max(1, std::min(32, atoi(e)));
   if (const char* e = getenv("PPLOAD_PDL")) L->pdl = atoi(e) != 0;
   if (const char* e = getenv("PPLOAD_GRID_PER_SM")) L->grid_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
+  L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
   L->linked = (L->W == 1);
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PP_ERR_CUDA, "create sync"));
@@ -490,7 +494,9 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   // Programmatic dependent launch only right after another gather of this epoch:
   // batches of one epoch are independent, and the first gather after a permute
   // or an event wait is fully serialised, so every gather sees a complete order.
-  PPL_CUDA(L, launch_gather(a, vec, L->pdl && L->last_was_gather, L->grid_per_sm, L->stream));
+  int path = vec ? kPathVector : kPathScalar;
+  if (vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && L->n_spill > 0))) path = kPathTma;
+  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_was_gather, L->grid_per_sm, L->stream));
   L->last_was_gather = !handoff;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));

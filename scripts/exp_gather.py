@@ -79,3 +79,54 @@ run(16, 1, 4, 8, 1)
 run(16, 1, 4, 299, 1)
 run(16, 1, 4, 8, 1, chunk=8192)
 run(16, 1, 4, 299, 1, chunk=8192)
+
+# --- bulk-copy (TMA) path vs register-staged LDG path, HBM and pinned-host stores
+def run_store(mode, budget, k, reps=3, chunk=1):
+    os.environ["PPLOAD_GATHER"] = mode
+    os.environ["PPLOAD_TILE_ROWS"] = "16"
+    L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
+                  hbm_budget_bytes=budget)
+    L.fill_synthetic(2504)
+    L.set_stream(stream)
+
+    def epoch(e):
+        L.epoch_permute(e, chunk, stream)
+        done = 0
+        while done < steps:
+            done += len(L.next_batches(min(k, steps - done), ring[done], slot, None, None, stream))
+
+    with torch.cuda.stream(stream):
+        epoch(0)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for i in range(reps):
+            epoch(1 + i)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    info = L.query()
+    L.close()
+    print(json.dumps(dict(mode=mode, budget=budget, k=k, chunk=chunk, epoch_ms=ms, nodes_per_s=N / ms * 1e3,
+                          rows_spill=info["rows_spill"], read_GBs=N * 1600 / ms / 1e6)), flush=True)
+
+
+for mode in ("ldg", "tma"):
+    run_store(mode, 0, 8, reps=10)
+    run_store(mode, 0, 299, reps=10)
+    run_store(mode, -1, 8)
+    run_store(mode, -1, 8, chunk=8192)
+# DMA reference: one 3.9 GB pinned host -> device copy
+h = torch.empty(N * 1600, dtype=torch.uint8, pin_memory=True)
+d = torch.empty_like(h, device="cuda")
+d.copy_(h, non_blocking=True)
+torch.cuda.synchronize()
+a = torch.cuda.Event(enable_timing=True)
+b = torch.cuda.Event(enable_timing=True)
+a.record()
+d.copy_(h, non_blocking=True)
+b.record()
+torch.cuda.synchronize()
+print(json.dumps(dict(dma_h2d_GBs=h.numel() / a.elapsed_time(b) / 1e6)), flush=True)

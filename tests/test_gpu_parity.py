@@ -440,3 +440,54 @@ def test_epoch_prefetch(pp, tiny):
             run_epoch(L, B, H, F, oracle.BF16)
             L.epoch_permute(e, 7)
             assert np.array_equal(L.get_order(), oracle.epoch_order(e, N, 7))
+
+
+@pytest.mark.parametrize("mode", ["ldg", "tma"])
+@pytest.mark.parametrize("case", ["bf16", "f16", "copy16", "spill", "loopback", "nodeset"])
+def test_gather_paths(pp, mode, case, monkeypatch):
+    # both vector kernels (register-staged LDG and bulk-copy TMA) against the oracle
+    monkeypatch.setenv("PPLOAD_GATHER", mode)
+    H, N, F, B = 4, 4099, 100, 512
+    out_dt = {"f16": oracle.F16, "copy16": oracle.F16}.get(case, oracle.BF16)
+    dt16 = case == "copy16"
+    X, hs, rs = hop_tensor(50, H, N, F, "hop_major", dtype=np.uint16 if dt16 else np.float32)
+    in_dt = oracle.F16 if dt16 else oracle.F32
+    bits = X if dt16 else X.view(np.uint32)
+    lab = make_labels(51, N)
+    kw = dict(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=in_dt,
+              batch_size=B, out_dtype=out_dt, labels=lab)
+    W = 2 if case == "loopback" else 1
+    S = make_node_set(52, N, 3001) if case == "nodeset" else None
+    if case == "spill":
+        kw["hbm_budget_bytes"] = 1500 * H * F * 4
+    if S is not None:
+        kw["node_set"] = S
+    if W > 1:
+        Ls = [pp.Loader(world_size=W, rank=r, peers=pp.PP_PEERS_LOOPBACK, **kw) for r in range(W)]
+        pp.pp_link_loopback([L.h for L in Ls])
+    else:
+        Ls = [pp.Loader(**kw)]
+    try:
+        n = S.shape[0] if S is not None else N
+        order = oracle.epoch_order(9, n, 32, node_set=S)
+        for r, L in enumerate(Ls):
+            L.epoch_permute(9, 32)
+            # three steps per launch into a ring, then single steps
+            steps = oracle.num_steps(n, B, W)
+            ring = torch.empty((3, B, H, F), dtype=TORCH_DT[out_dt], device="cuda")
+            labs = torch.empty((3, B), dtype=torch.int32, device="cuda")
+            nodes = torch.empty((3, B), dtype=torch.int64, device="cuda")
+            t = 0
+            while t < steps:
+                rows = L.next_batches(3, ring, B * H * F * 2, labs, nodes)
+                torch.cuda.synchronize()
+                for i, nr in enumerate(rows):
+                    want, wl, wn = oracle.batch(bits, in_dt, hs, rs, H, F, order, B, W, t + i, r, out_dt, lab)
+                    assert nr == want.shape[0]
+                    assert np.array_equal(bits_of(ring[i, :nr], out_dt), want), (case, mode, t + i)
+                    assert np.array_equal(labs[i, :nr].cpu().numpy(), wl)
+                    assert np.array_equal(nodes[i, :nr].cpu().numpy(), wn)
+                t += len(rows)
+    finally:
+        for L in Ls:
+            L.close()
