@@ -204,9 +204,10 @@ def run_ours(args):
     steps = info["steps_per_epoch"]
     rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
 
-    # output ring: one slot per step of the epoch (> L2: outputs really go to DRAM)
-    ring = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
+    # output ring: one slot per step of the epoch, capped at 4 GB (>= 1 GB >> L2: outputs go to DRAM)
     slot_bytes = B * H * F * 2
+    nslots = min(steps, max(args.per_call, int(4e9 // slot_bytes)))
+    ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
     # rows this rank assembles per epoch (for the algorithmic bytes)
     my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
     U = -(-N // chunk)
@@ -223,11 +224,13 @@ def run_ours(args):
                 ev_mid.record(stream)
             done = 0
             while done < steps:
+                s0 = done % nslots
                 if k == 1:
-                    L.next_batch(ring[done], None, None, stream)
+                    L.next_batch(ring[s0], None, None, stream)
                     done += 1
                 else:
-                    done += len(L.next_batches(min(k, steps - done), ring[done], slot_bytes, None, None, stream))
+                    n = min(k, steps - done, nslots - s0)
+                    done += len(L.next_batches(n, ring[s0], slot_bytes, None, None, stream))
 
         with torch.cuda.stream(stream):
             for e in range(args.warmup):
@@ -259,7 +262,10 @@ def run_ours(args):
             tt = torch.tensor(t, device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.tolist()
-        launches = -(-steps // k)
+        launches, done = 0, 0  # gather launches per epoch (calls never wrap the ring)
+        while done < steps:
+            done += 1 if k == 1 else min(k, steps - done, nslots - done % nslots)
+            launches += 1
         per_launch_ms = t[1] / (nsteps * launches)
         bytes_per_launch = my_rows * (rec_in + rec_out + 4) / launches
         return {"total_ms": t[0], "gather_ms": t[1], "perm_ms": t[2], "per_launch_ms": per_launch_ms,
@@ -271,20 +277,29 @@ def run_ours(args):
     ms_per_step = m["total_ms"] / args.steps
     value = N * args.steps / (m["total_ms"] / 1e3)  # all ranks together assemble N rows per epoch
     peak, peak_kind = peaks()
-    roofline = {"bound": "hbm", "achieved": m["achieved"], "peak": peak, "unit": "GB/s", "frac": m["achieved"] / peak,
-                "traffic": committed_traffic(f"gather_{name}_k{k}"), "kernel": "k_gather_vec<bf16>",
-                "peak_kind": peak_kind, "per_launch_us": m["per_launch_ms"] * 1e3,
-                "algorithmic_bytes_per_launch": m["bytes_per_launch"],
-                "algorithmic_bytes_per_node": rec_in + rec_out + 4,
-                "frac_of_8TBs_nominal": m["achieved"] / 8000.0,
-                "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
-                        "(includes launch gaps and the overlapped next-epoch permutation)"}
+    if W == 1:
+        roofline = {"bound": "hbm", "achieved": m["achieved"], "peak": peak, "unit": "GB/s",
+                    "frac": m["achieved"] / peak, "traffic": committed_traffic(f"gather_{name}_k{k}"),
+                    "kernel": "k_gather_vec<bf16>", "peak_kind": peak_kind,
+                    "algorithmic_bytes_per_node": rec_in + rec_out + 4,
+                    "frac_of_8TBs_nominal": m["achieved"] / 8000.0}
+    else:
+        # pull design: (W-1)/W of each rank's rows arrive over NVLink as fp32 records
+        nvl = m["bytes_per_launch"] / (rec_in + rec_out + 4) * rec_in * (W - 1) / W
+        achieved = nvl / (m["per_launch_ms"] / 1e3) / 1e9
+        roofline = {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s", "frac": achieved / 770.0,
+                    "traffic": None, "kernel": "k_gather_tma<bf16, sharded>",
+                    "peak_kind": "guide-measured peer copy per direction (B200_PROFILING.md)",
+                    "algorithmic_nvlink_bytes_per_node": rec_in * (W - 1) / W, "hbm_GBs": m["achieved"]}
+    roofline.update({"per_launch_us": m["per_launch_ms"] * 1e3, "algorithmic_bytes_per_launch": m["bytes_per_launch"],
+                     "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
+                             "(includes launch gaps and the overlapped next-epoch permutation)"})
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if W == 1 else "strong",
         "vs_baseline": None, "dtype": "f32->bf16", "data": "synthetic (§8(d) generator G, filled in place)",
         "config": config_dict(name, cfg, W, "inputs > L2 (3.9 GB store), outputs rotate over a "
-                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring (one slot per step)"),
+                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring of {nslots} slots"),
         "roofline": roofline, "gpu_launches": (perm_kernels + m["launches"]) * args.steps, "clocks": m["clocks"],
         "batches_per_launch": k, "prefetch_next_epoch_order": bool(args.prefetch),
     }
