@@ -25,6 +25,7 @@ struct SortScratch {
   uint32_t* blocksums;  // [ceil((nb+1)/kScanTile)]
   uint32_t* tmp;        // [U]       unit ids grouped by bucket
   uint32_t* ragged;     // [1]       position of the ragged chunk in pi
+  uint32_t k32_mask = 0xffffffffu;  // test knob: compare fewer sub-key bits (forces the tie path)
 };
 constexpr int kScanTile = 4096;
 

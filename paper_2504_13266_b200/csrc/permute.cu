@@ -141,26 +141,65 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t* __restrict
   }
 }
 
+// Four units per thread per trip so four returning atomics are in flight.
+constexpr int kScatterIlp = 4;
+
 __global__ void k_scatter(uint64_t seed, uint32_t U, int bits, uint32_t* __restrict__ cursor,
                           uint32_t* __restrict__ tmp) {
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-    const uint32_t slot = atomicAdd(&cursor[bucket_of(unit_sort_key(seed, u), bits)], 1u);
-    tmp[slot] = u;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t u0 = blockIdx.x * blockDim.x + threadIdx.x; u0 < U; u0 += stride * kScatterIlp) {
+    uint32_t slot[kScatterIlp];
+#pragma unroll
+    for (int q = 0; q < kScatterIlp; ++q) {
+      const uint32_t u = u0 + q * stride;
+      if (u < U) slot[q] = atomicAdd(&cursor[bucket_of(unit_sort_key(seed, u), bits)], 1u);
+    }
+#pragma unroll
+    for (int q = 0; q < kScatterIlp; ++q) {
+      const uint32_t u = u0 + q * stride;
+      if (u < U) tmp[slot[q]] = u;
+    }
   }
 }
 
 // One warp per bucket.  Lane l holds unit i = ibase + l; its rank is the
 // number of (key, id) pairs in the bucket that compare below its own, counted
-// by broadcasting 32 candidates at a time with __shfl_sync.  Buckets of any
-// size are handled (tiles of 32 x 32); the common case is a single tile.
+// by broadcasting candidates with __shfl_sync.  Buckets of <= 32 units (all
+// but ~0.3 %) compare only the 32 key bits below the bucket prefix, falling
+// back to the full (key, id) order when two of them tie; larger buckets use
+// tiles of 32 x 32 with full compares.
 __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32_t* __restrict__ offsets,
-                                                     uint32_t nb, const uint32_t* __restrict__ tmp,
+                                                     uint32_t nb, int bits, uint32_t k32_mask,
+                                                     const uint32_t* __restrict__ tmp,
                                                      uint32_t* __restrict__ pi) {
   const uint32_t bucket = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (bucket >= nb) return;  // warp-uniform
   const uint32_t beg = offsets[bucket];
   const uint32_t n = offsets[bucket + 1] - beg;
+  if (n <= 32) {
+    const bool vi = lane < static_cast<int>(n);
+    const uint32_t ui = vi ? tmp[beg + lane] : 0xffffffffu;
+    const uint64_t ki = vi ? unit_sort_key(seed, ui) : ~0ull;
+    const uint32_t k32 = static_cast<uint32_t>((ki << bits) >> 32) & k32_mask;  // bits below the bucket prefix
+    uint32_t rank = 0, eq = 0;
+#pragma unroll 4
+    for (uint32_t s = 0; s < n; ++s) {
+      const uint32_t kk = __shfl_sync(0xffffffffu, k32, s);
+      rank += kk < k32;
+      eq += kk == k32;
+    }
+    if (__any_sync(0xffffffffu, vi && eq > 1)) {  // a 32-bit tie: full (key, id) order
+      rank = 0;
+      for (uint32_t s = 0; s < n; ++s) {
+        const uint64_t kk = __shfl_sync(0xffffffffu, ki, s);
+        const uint32_t uu = __shfl_sync(0xffffffffu, ui, s);
+        rank += (kk < ki) | ((kk == ki) & (uu < ui));
+      }
+    }
+    if (vi) pi[beg + rank] = ui;
+    return;
+  }
   for (uint32_t ibase = 0; ibase < n; ibase += 32) {
     const bool vi = ibase + lane < n;
     const uint32_t ui = vi ? tmp[beg + ibase + lane] : 0xffffffffu;
@@ -258,7 +297,7 @@ cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool al
   k_scan_down<<<nblk, kScanThreads, 0, st>>>(s.counts, n, s.blocksums, s.cursor);
   k_scatter<<<unit_blocks, threads, 0, st>>>(seed, U, bits, s.cursor, s.tmp);
   const uint64_t rank_threads = static_cast<uint64_t>(nb) * 32;
-  k_bucket_rank<<<static_cast<uint32_t>((rank_threads + 255) / 256), 256, 0, st>>>(seed, s.counts, nb, s.tmp, pi);
+  k_bucket_rank<<<static_cast<uint32_t>((rank_threads + 255) / 256), 256, 0, st>>>(seed, s.counts, nb, bits, s.k32_mask, s.tmp, pi);
   if (ragged != nullptr) k_find_ragged<<<std::min<uint32_t>((U + 255) / 256, 148u * 8u), 256, 0, st>>>(pi, U, ragged);
   return cudaGetLastError();
 }

@@ -165,6 +165,14 @@ cudaError_t copy_in(const pp_loader* L, const pp_hop_desc& h, int64_t row0, int6
   return cudaSuccess;
 }
 
+// The prefetched permutation runs at the lowest stream priority so the block
+// scheduler serves the current epoch's gathers first.
+int prefetch_priority() {
+  int least = 0, greatest = 0;
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+  return least;
+}
+
 pp_status validate(const pp_loader_desc* d) {
   if (!d) return fail(PP_ERR_INVALID, "desc is NULL");
   const pp_hop_desc& h = d->hops;
@@ -326,12 +334,16 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
       cudaEventCreateWithFlags(&L->ev_out, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_pref, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_pref_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&L->pstream, cudaStreamNonBlocking) != cudaSuccess)
+      cudaStreamCreateWithPriority(&L->pstream, cudaStreamNonBlocking, prefetch_priority()) != cudaSuccess)
     return bail(fail(PP_ERR_CUDA, "event creation"));
   cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, L->dev);
   if (const char* e = getenv("PPLOAD_TILE_ROWS")) L->tile_rows = std::max(1, std::min(32, atoi(e)));
   if (const char* e = getenv("PPLOAD_PDL")) L->pdl = atoi(e) != 0;
   if (const char* e = getenv("PPLOAD_GRID_PER_SM")) L->grid_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("PPLOAD_DEBUG_TIE_BITS")) {  // test knob: keep only the top n sub-key bits
+    const int n = std::max(1, std::min(32, atoi(e)));
+    L->sort.k32_mask = n == 32 ? 0xffffffffu : ~((1u << (32 - n)) - 1u);
+  }
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
