@@ -186,6 +186,22 @@ pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride
                           int32_t* out_labels, int64_t* out_nodes, int32_t* rows,
                           int32_t* n_done, void* consumer_stream);
 
+/* Consumer fusion: assemble the next n steps AND apply
+ * SIGN's per-hop linear layer ("learns R+1 weight matrices for each hop",
+ * PAPER.md:184-185) in one tensor-core kernel:
+ *   Z[j, k, :] = bf16_rne(X_k[v_j, :]) @ W_k      (fp32 accumulation)
+ * The batch itself is never written to memory.
+ *   W: device bf16 [H][F][D] row-major (W_k = W[k] is F x D), 16-B aligned.
+ *   D: 256 or 512.  Requires an fp32, HBM-resident (no spill) store with
+ *      F <= 128, F % 4 == 0, and W == 1.
+ *   Z: device [n][B][H][D] of z_dtype (PP_BF16: RNE from fp32, or PP_F32),
+ *      slot pitch z_stride_bytes (>= B*H*D*elem when n > 1), 16-B aligned.
+ * Cursor, rows[], n_done and stream semantics as pp_next_batches.
+ * Errors: PP_ERR_INVALID (unsupported loader or shapes), PP_ERR_STATE,
+ * PP_END_OF_EPOCH, PP_ERR_CUDA. */
+pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,
+                                 int64_t z_stride_bytes, int32_t* rows, int32_t* n_done, void* consumer_stream);
+
 /* Move the cursor to step t (0 <= t <= steps_per_epoch): resume support.
  * (seed, chunk, cursor) is the loader's whole epoch state. */
 pp_status pp_seek(pp_loader* L, int64_t step);

@@ -260,3 +260,22 @@ def tiny_hops(data_seed: int = 2504, n: int = 2708, m: int = 5429, F: int = 128,
     src, dst = gen_graph(data_seed, n, m)
     X0 = gen_rows(data_seed, F32, 1, F, np.arange(n)).reshape(n, F).view(np.float32)
     return propagate_graph(n, src, dst, X0, K)
+
+
+# --------------------------------------------------------------------------- §8(f)-1 consumer: per-hop linear
+def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns -> exact float64 values (a bf16 is the top half of an fp32)."""
+    return (np.asarray(bits, dtype=np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def hop_linear(batch_bits: np.ndarray, W_bits: np.ndarray):
+    """SIGN's per-hop linear layer (one weight matrix per hop) on a batch:
+    Z[j, k, :] = X[j, k, :] @ W[k] in float64 from the exact bf16 values (numpy matmul as the
+    library step).  batch_bits: bf16 bits [rows, H, F] (the oracle batch, O10); W_bits: bf16 bits
+    [H, F, D].  Returns (Z, S) with S[j, k, :] = |X[j, k, :]| @ |W[k]| (the scale of the
+    rounding-error bound of any summation order)."""
+    X = bf16_bits_to_f64(batch_bits)
+    Wf = bf16_bits_to_f64(W_bits)
+    Z = np.einsum("jkf,kfd->jkd", X, Wf)
+    S = np.einsum("jkf,kfd->jkd", np.abs(X), np.abs(Wf))
+    return Z, S

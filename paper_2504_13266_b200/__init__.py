@@ -26,7 +26,7 @@ __all__ = [
     "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_epoch_prefetch", "pp_next_batch", "pp_next_batches",
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
-    "pp_import_peer_stores", "pp_debug_set_sort_bits_delta",
+    "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear",
 ]
 
 
@@ -154,6 +154,16 @@ def pp_next_batches(h, n, out, out_stride_bytes, out_labels=None, out_nodes=None
     return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
 
 
+def pp_next_batches_linear(h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream=None):
+    """Fused batch assembly + per-hop linear (tensor cores).  Returns rows per step ([] at epoch end)."""
+    rows = (ctypes.c_int32 * n)()
+    done = ctypes.c_int32()
+    rc = lib().pp_next_batches_linear(h, n, _ptr(W), D, _ptr(Z), _dtype(z_dtype), z_stride_bytes, rows,
+                                      ctypes.byref(done), _stream(consumer_stream))
+    _check(rc, "pp_next_batches_linear", ok=(PP_OK, PP_END_OF_EPOCH))
+    return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
+
+
 def pp_seek(h, step: int) -> None:
     _check(lib().pp_seek(h, step), "pp_seek")
 
@@ -241,6 +251,9 @@ class Loader:
 
     def next_batches(self, n, out, out_stride_bytes, out_labels=None, out_nodes=None, consumer_stream=None):
         return pp_next_batches(self.h, n, out, out_stride_bytes, out_labels, out_nodes, consumer_stream)
+
+    def next_batches_linear(self, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream=None):
+        return pp_next_batches_linear(self.h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream)
 
     def seek(self, step):
         pp_seek(self.h, step)

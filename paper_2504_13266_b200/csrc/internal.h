@@ -74,6 +74,24 @@ cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_
 bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride);
 bool gather_tma_ok(int32_t HF, int32_t in_dtype);  // record fits the bulk-copy stages
 
+// ---- fused gather + per-hop linear on tcgen05 (linear.cu) --------------------
+struct LinearArgs {
+  const uint32_t* order;
+  const int64_t* node_set;
+  const uint8_t* store;     // HBM store, node-major fp32 records
+  int64_t rec_stride;
+  int64_t N, first_pos, step_stride;
+  int32_t B, nsteps;
+  const void* W;            // bf16 [H][F][D]
+  int32_t H, F, D;
+  uint8_t* Z;               // [nsteps][B][H][D] of z_elem bytes
+  int64_t z_stride;         // bytes between step slots
+  int32_t z_elem;           // 2 (bf16) or 4 (fp32)
+  int32_t num_sms;
+};
+bool linear_supported(int H, int F, int D, int num_sms);
+cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st);
+
 // ---- synthetic fill (gather.cu) ---------------------------------------------
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
                                   int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,

@@ -536,6 +536,67 @@ pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride
   return next_steps(L, n, out, out_stride_bytes, out_labels, out_nodes, rows, n_done, consumer_stream);
 }
 
+pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,
+                                 int64_t z_stride_bytes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (!rows || n < 1 || !W || !Z) return fail(PP_ERR_INVALID, "NULL argument or n < 1");
+  if (L->in_dtype != PP_F32 || L->n_spill > 0 || L->W != 1)
+    return fail(PP_ERR_INVALID, "fused linear needs an fp32, HBM-resident, unsharded store");
+  if (!linear_supported(L->H, L->F, D, L->num_sms))
+    return fail(PP_ERR_INVALID, "fused linear supports F <= 128 with F %% 4 == 0 and D in {256, 512} (F=%d, D=%d)",
+                L->F, D);
+  if (z_dtype != PP_BF16 && z_dtype != PP_F32) return fail(PP_ERR_INVALID, "z_dtype must be PP_BF16 or PP_F32");
+  if (reinterpret_cast<uintptr_t>(W) % 16 || reinterpret_cast<uintptr_t>(Z) % 16 || z_stride_bytes % 16)
+    return fail(PP_ERR_INVALID, "W, Z and z_stride_bytes must be 16-byte aligned");
+  const int z_elem = z_dtype == PP_F32 ? 4 : 2;
+  if (n > 1 && z_stride_bytes < L->B * L->H * static_cast<int64_t>(D) * z_elem)
+    return fail(PP_ERR_INVALID, "z_stride_bytes smaller than one step");
+  if (!L->permuted) return fail(PP_ERR_STATE, "pp_next_batches_linear before pp_epoch_permute");
+  if (L->cursor >= L->steps) {
+    rows[0] = 0;
+    if (n_done) *n_done = 0;
+    return PP_END_OF_EPOCH;
+  }
+  const int64_t nsteps = std::min<int64_t>(n, L->steps - L->cursor);
+  DevGuard g(L->dev);
+  cudaStream_t cons = static_cast<cudaStream_t>(consumer_stream);
+  const bool handoff = cons != L->stream;
+  if (handoff) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+  }
+  LinearArgs a{};
+  a.order = L->d_order;
+  a.node_set = L->d_node_set;
+  a.store = L->d_store;
+  a.rec_stride = L->rec_stride;
+  a.N = L->N;
+  a.first_pos = L->cursor * L->B;
+  a.step_stride = L->B;
+  a.B = static_cast<int32_t>(L->B);
+  a.nsteps = static_cast<int32_t>(nsteps);
+  a.W = W;
+  a.H = L->H;
+  a.F = L->F;
+  a.D = D;
+  a.Z = static_cast<uint8_t*>(Z);
+  a.z_stride = z_stride_bytes;
+  a.z_elem = z_elem;
+  a.num_sms = L->num_sms;
+  PPL_CUDA(L, launch_gather_linear(a, L->stream));
+  L->last_was_gather = false;
+  if (handoff) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+    PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
+  }
+  for (int64_t i = 0; i < nsteps; ++i)
+    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - (L->cursor + i) * L->B)));
+  L->cursor += nsteps;
+  if (n_done) *n_done = static_cast<int32_t>(nsteps);
+  return PP_OK;
+}
+
 pp_status pp_seek(pp_loader* L, int64_t step) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (!L->permuted) return fail(PP_ERR_STATE, "pp_seek before pp_epoch_permute");
