@@ -88,6 +88,8 @@ struct LinearArgs {
   int64_t z_stride;         // bytes between step slots
   int32_t z_elem;           // 2 (bf16) or 4 (fp32)
   int32_t num_sms;
+  int32_t debug;            // experiment knob (PPLOAD_DEBUG_LINEAR): 1 skip loads, 2 skip Z stores
+  uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null
 };
 bool linear_supported(int H, int F, int D, int num_sms);
 cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st);

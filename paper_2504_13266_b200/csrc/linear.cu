@@ -33,12 +33,20 @@ namespace ppl {
 
 namespace {
 
-constexpr int kLinThreads = 384;   // 12 warps
+constexpr int kEpiWarps = 4;       // one per TMEM lane quadrant (8 measured slower: register spills)
+constexpr int kLinThreads = (12 + kEpiWarps) * 32;  // 0-7 producers, 8 MMA, 9-11 idle, 12.. epilogue
+constexpr int kProducerWarps = 8;
+constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kMmaWarp = 8;
+constexpr int kEpiWarp0 = 12;      // warps 12..19: TMEM lane quadrant warp % 4, column group (warp-12)/4
+constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kTileM = 128;        // batch rows per tile (UMMA M)
 constexpr int kUmmaN = 256;        // columns per accumulator (UMMA N)
+constexpr int kEpiCols = kUmmaN / (kEpiWarps / 4);  // accumulator columns drained per epilogue warp
 constexpr int kKPad = 128;         // F zero-padded to two 64-element K blocks
 constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
 constexpr int kStages = 2;
+constexpr int kStagePitch = 128;   // epilogue staging row pitch (16-byte chunks XOR-swizzled by row)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -115,6 +123,16 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])    \
       : "r"(taddr))
 
+// Experiment probe (LinearArgs::ts, PPLOAD_DEBUG_TS): %globaltimer at named
+// points of CTA 0's first kDbgTiles tiles, kDbgSlots per tile.
+constexpr int kDbgTiles = 24, kDbgSlots = 14;
+__device__ __forceinline__ void dbg_ts(const LinearArgs& a, int tile, int slot, int) {
+  if (tile >= kDbgTiles) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  a.ts[tile * kDbgSlots + slot] = t;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearArgs a) {
@@ -123,8 +141,9 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
   const int D = a.D;
   uint8_t* w_s = smem;                                // [2 kb][D rows][128 B]
   uint8_t* a_s = smem + 2 * D * 128;                  // [kStages][2 kb][128 rows][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(a_s + kStages * kABytes);
-  uint64_t* a_full = bars;                            // [kStages], 128 producer arrivals
+  uint8_t* z_s = a_s + kStages * kABytes;             // [8 epilogue warps][32 rows][80 B] staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * 32 * kStagePitch);
+  uint64_t* a_full = bars;                            // [kStages], kProducerThreads arrivals
   uint64_t* a_empty = bars + kStages;                 // [kStages], MMA commit
   uint64_t* t_full = bars + 2 * kStages;              // [2], MMA commit
   uint64_t* t_empty = bars + 2 * kStages + 2;         // [2], 128 epilogue arrivals
@@ -138,33 +157,35 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      bar_init(&a_full[s], 128);
+      bar_init(&a_full[s], kProducerThreads);
       bar_init(&a_empty[s], 1);
     }
     for (int h = 0; h < 2; ++h) {
       bar_init(&t_full[h], 1);
-      bar_init(&t_empty[h], 128);
+      bar_init(&t_empty[h], kEpiThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {  // TMEM: 512 fp32 columns x 128 lanes (two 256-column accumulators)
+  if (warp == kMmaWarp) {  // TMEM: 512 fp32 columns x 128 lanes (two 256-column accumulators)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // W_k^T into shared memory: B operand row n = output column d, K index = f
   // (zero for f >= F).  Consecutive threads take consecutive d: coalesced reads.
-  const __nv_bfloat16* wk = reinterpret_cast<const __nv_bfloat16*>(a.W) + static_cast<int64_t>(k) * F * D;
-  for (int idx = threadIdx.x; idx < D * 16; idx += kLinThreads) {
-    const int d = idx % D, c = idx / D, kb = c >> 3, cc = c & 7;
-    uint16_t v[8];
+  // Each thread reads 8 consecutive d of one f with a 16-byte load and
+  // scatters them as 2-byte elements into 8 K-major rows; consecutive lanes
+  // take consecutive f so the 2-byte shared stores of a warp are contiguous.
+  const uint8_t* wk = static_cast<const uint8_t*>(a.W) + static_cast<int64_t>(k) * F * D * 2;
+  for (int idx = threadIdx.x; idx < kKPad * (D / 8); idx += kLinThreads) {
+    const int f = idx % kKPad, d0 = (idx / kKPad) * 8;
+    const uint4 w = f < F ? *reinterpret_cast<const uint4*>(wk + (static_cast<int64_t>(f) * D + d0) * 2)
+                          : make_uint4(0, 0, 0, 0);
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    const int kb = f >> 6, cc = (f >> 3) & 7, fo = (f & 7) * 2;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int f = kb * 64 + cc * 8 + j;
-      v[j] = f < F ? __bfloat16_as_ushort(wk[static_cast<int64_t>(f) * D + d]) : 0;
-    }
-    const uint4 y = make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16),
-                               v[4] | (uint32_t(v[5]) << 16), v[6] | (uint32_t(v[7]) << 16));
-    *reinterpret_cast<uint4*>(w_s + kb * D * 128 + sw128(d, cc)) = y;
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint16_t*>(w_s + kb * D * 128 + sw128(d0 + j, cc) + fo) =
+          static_cast<uint16_t>(wv[j >> 1] >> ((j & 1) * 16));
   }
   fence_async_smem();
   tc_fence_before();
@@ -183,44 +204,73 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
     return static_cast<int>(min(static_cast<int64_t>(kTileM), nrows - r0));
   };
 
-  if (warp < 4) {
-    // ---------------- producers: gather + cast into the swizzled A tile
-    const int r = threadIdx.x;  // 0..127
-    int i = 0;
-    for (int64_t t = q; t < total; t += Q) {
+  if (warp < kProducerWarps) {
+    // ---------------- producers: gather + cast into the swizzled A tile.
+    // Warp w owns tile rows 16w..16w+15; for each row the 32 lanes load the
+    // row's hop-k vector as consecutive 16-byte pieces (one coalesced request
+    // per row, lane l = fp32 elements 4l..4l+3, zero past F); all 16 rows are
+    // in flight before any is converted.  Even lanes then pair with their odd
+    // neighbour to form one 16-byte chunk of 8 bf16 = K elements 8c..8c+7.
+    const int rbase = warp * 16;
+    auto next_tile = [&](int64_t t) -> int64_t {  // first non-empty tile at or after t
+      for (; t < total; t += Q) {
+        int64_t st_, ps_;
+        int r_;
+        if (tile_rows(t, st_, r_, ps_) > 0) return t;
+      }
+      return total;
+    };
+    // Lane layout: half-warp hw = lane / 16 takes row 2 it + hw of iteration it,
+    // lane c = lane % 16 the K chunk 8c..8c+7 (two 16-byte fp32 loads -> one
+    // 16-byte bf16 store), so no shuffles are needed to pair elements.
+    const int hw = lane >> 4, c = lane & 15;
+    auto load_tile = [&](int64_t t, uint4(&x)[16]) {
       int64_t step, pos;
       int r0;
       const int rows = tile_rows(t, step, r0, pos);
-      if (rows <= 0) continue;
-      const int s = i & 1;
-      bar_wait(&a_empty[s], ((i >> 1) & 1) ^ 1);
-      uint8_t* at = a_s + s * kABytes;
-      const uint8_t* src = nullptr;
-      if (r < rows) {
-        uint64_t v = a.order[pos + r0 + r];
+      const uint8_t* my_src = nullptr;  // lane j < 16 resolves row rbase + j
+      if (lane < 16 && rbase + lane < rows) {
+        uint64_t v = a.order[pos + r0 + rbase + lane];
         if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
-        src = a.store + static_cast<int64_t>(v) * a.rec_stride + static_cast<int64_t>(k) * F * 4;
+        my_src = a.store + static_cast<int64_t>(v) * a.rec_stride + static_cast<int64_t>(k) * F * 4;
       }
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb) {
-        uint4 x[16];
+      for (int it = 0; it < 8; ++it) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_src), 2 * it + hw));
+        const bool on = src != nullptr && !(a.debug & 1);
+        // K block 0: elements 4c..4c+3, K block 1: 64+4c..64+4c+3 (each load 256 contiguous bytes per half-warp)
+        x[2 * it] = (on && 4 * c < F) ? ldg16(src + c * 16) : make_uint4(0, 0, 0, 0);
+        x[2 * it + 1] = (on && 64 + 4 * c < F) ? ldg16(src + 256 + c * 16) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0;
+    auto store_tile = [&](int i, const uint4(&x)[16]) {
+      const int s = i & 1;
+      if (dbg_lane) dbg_ts(a, i, 0, 0);
+      bar_wait(&a_empty[s], ((i >> 1) & 1) ^ 1);
+      if (dbg_lane) dbg_ts(a, i, 1, 0);
+      uint8_t* at = a_s + s * kABytes;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {  // 16 x 4 fp32 = this K block's 64 elements
-          const int f = kb * 64 + j * 4;
-          x[j] = (src != nullptr && f < F) ? ldg16(src + f * 4) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const uint4 y = make_uint4(bf16x2(x[2 * cc].x, x[2 * cc].y), bf16x2(x[2 * cc].z, x[2 * cc].w),
-                                     bf16x2(x[2 * cc + 1].x, x[2 * cc + 1].y), bf16x2(x[2 * cc + 1].z, x[2 * cc + 1].w));
-          *reinterpret_cast<uint4*>(at + kb * (kTileM * 128) + sw128(r, cc)) = y;
-        }
+      for (int it = 0; it < ((a.debug & 8) ? 0 : 8); ++it) {
+        const uint4 x0 = x[2 * it], x1 = x[2 * it + 1];
+        const int r = rbase + 2 * it + hw;
+        // 4 bf16 = 8 bytes: half (c & 1) of 16-byte chunk c >> 1, in K block 0 and K block 1
+        const uint32_t off = sw128(r, c >> 1) + (c & 1) * 8;
+        *reinterpret_cast<uint2*>(at + off) = make_uint2(bf16x2(x0.x, x0.y), bf16x2(x0.z, x0.w));
+        *reinterpret_cast<uint2*>(at + kTileM * 128 + off) = make_uint2(bf16x2(x1.x, x1.y), bf16x2(x1.z, x1.w));
       }
       fence_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
       bar_arrive(&a_full[s]);
-      ++i;
+      if (dbg_lane) dbg_ts(a, i, 2, 0);
+    };
+    uint4 x[16];
+    int i = 0;
+    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+      load_tile(t, x);
+      store_tile(i++, x);
     }
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (one lane)
     if (lane == 0) {
       int i = 0;
@@ -229,12 +279,15 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
         int r0;
         if (tile_rows(t, step, r0, pos) <= 0) continue;
         const int s = i & 1;
+        const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0;
         bar_wait(&a_full[s], (i >> 1) & 1);
         tc_fence_after();
+        if (dbg_lane) dbg_ts(a, i, 3, 0);
         const uint8_t* at = a_s + s * kABytes;
         for (int h = 0; h < nh; ++h) {
           bar_wait(&t_empty[h], (i & 1) ^ 1);
           tc_fence_after();
+          if (dbg_lane) dbg_ts(a, i, 4 + 2 * h, 0);
 #pragma unroll
           for (int ks = 0; ks < kKPad / 16; ++ks) {
             const int kb = ks >> 2, j = ks & 3;
@@ -243,16 +296,25 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
             umma(tmem + h * kUmmaN, ad, bd, ks > 0 ? 1u : 0u);
           }
           umma_commit(&t_full[h]);
+          if (dbg_lane) dbg_ts(a, i, 5 + 2 * h, 0);
         }
         umma_commit(&a_empty[s]);  // the A stage is free once these MMAs have read it
         ++i;
       }
     }
     __syncwarp();
-  } else if (warp >= 8) {
-    // ---------------- epilogue: TMEM -> registers -> Z
-    const int e = warp & 3;  // TMEM lane quadrant of this warp
-    const int row = e * 32 + lane;
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue: TMEM -> registers -> shared staging -> Z.
+    // One warp per TMEM lane quadrant (warp % 4); lane l holds row 32e + l
+    // after tcgen05.ld.  Each 128-byte slice of the 32 rows (64 bf16 / 32 fp32
+    // columns) is staged with 16-byte chunks XOR-swizzled by row (conflict-free)
+    // and written back with every store covering 4 rows x 128 contiguous bytes.
+    const int e = warp & 3;                          // TMEM lane quadrant
+    const int g = (warp - kEpiWarp0) >> 2;           // column group: [g*kEpiCols, (g+1)*kEpiCols) of each 256
+    uint8_t* sbase = z_s + (warp - kEpiWarp0) * 32 * kStagePitch;
+    uint8_t* my = sbase + lane * kStagePitch;
+    const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
+    const int cols_per_slice = 128 / a.z_elem;
     int i = 0;
     for (int64_t t = q; t < total; t += Q) {
       int64_t step, pos;
@@ -262,42 +324,62 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
       for (int h = 0; h < nh; ++h) {
         bar_wait(&t_full[h], i & 1);
         tc_fence_after();
-        uint8_t* zrow = a.Z + step * a.z_stride +
-                        ((static_cast<int64_t>(r0 + row) * H + k) * D + h * kUmmaN) * a.z_elem;
+        if (dbg_lane) dbg_ts(a, i, 12 + h, 0);
 #pragma unroll 1
-        for (int c0 = 0; c0 < kUmmaN; c0 += 32) {
-          uint32_t v[32];
-          PPL_TMEM_LD32(tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN + c0, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (row < rows) {
+        for (int c0 = g * kEpiCols; c0 < ((a.debug & 4) ? g * kEpiCols : (g + 1) * kEpiCols); c0 += cols_per_slice) {
+          for (int c1 = 0; c1 < cols_per_slice; c1 += 32) {  // one tcgen05.ld of 32 columns
+            uint32_t v[32];
+            PPL_TMEM_LD32(tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN + c0 + c1, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int chunk0 = c1 * a.z_elem / 16;  // first 16-byte chunk of this piece in the slice
             if (a.z_elem == 2) {
-              uint4* dst = reinterpret_cast<uint4*>(zrow + c0 * 2);
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                dst[j] = make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                                    bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+                *reinterpret_cast<uint4*>(my + (((chunk0 + j) ^ (lane & 7)) << 4)) =
+                    make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
             } else {
-              uint4* dst = reinterpret_cast<uint4*>(zrow + c0 * 4);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my + (((chunk0 + j) ^ (lane & 7)) << 4)) =
+                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
           }
+          __syncwarp();
+          {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {  // 4 rows x 128 contiguous bytes per instruction
+              const int rr = it * 4 + (lane >> 3), ch = lane & 7;
+              const uint4 y = *reinterpret_cast<const uint4*>(sbase + rr * 128 + ((ch ^ (rr & 7)) << 4));
+              if (e * 32 + rr < rows && !(a.debug & 2)) {
+                uint8_t* d = a.Z + step * a.z_stride +
+                             ((static_cast<int64_t>(r0 + e * 32 + rr) * H + k) * D + h * kUmmaN + c0) * a.z_elem +
+                             ch * 16;
+                *reinterpret_cast<uint4*>(d) = y;
+              }
+            }
+            __syncwarp();
+          }
         }
+        if (dbg_lane) dbg_ts(a, i, 8 + 2 * h, 0);
         tc_fence_before();
         bar_arrive(&t_empty[h]);
+        if (dbg_lane) dbg_ts(a, i, 9 + 2 * h, 0);
       }
       ++i;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
-size_t linear_smem_bytes(int D) { return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + 128; }
+size_t linear_smem_bytes(int D) {
+  return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + kEpiWarps * 32 * kStagePitch + 128;
+}
 
 bool linear_supported(int H, int F, int D, int num_sms) {
   return F >= 1 && F <= kKPad && F % 4 == 0 && (D == 256 || D == 512) && H >= 1 && H <= num_sms;

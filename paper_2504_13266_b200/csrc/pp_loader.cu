@@ -584,7 +584,27 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.z_stride = z_stride_bytes;
   a.z_elem = z_elem;
   a.num_sms = L->num_sms;
+  if (const char* e = getenv("PPLOAD_DEBUG_LINEAR")) a.debug = atoi(e);
+  static uint64_t* dbg_ts = nullptr;  // experiment probe: timestamps of CTA 0 (PPLOAD_DEBUG_TS=1)
+  const bool want_ts = getenv("PPLOAD_DEBUG_TS") != nullptr;
+  if (want_ts && !dbg_ts) PPL_CUDA(L, cudaMalloc(&dbg_ts, 24 * 14 * 8));
+  if (want_ts) {
+    PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, 24 * 14 * 8, L->stream));
+    a.ts = dbg_ts;
+  }
   PPL_CUDA(L, launch_gather_linear(a, L->stream));
+  if (want_ts) {
+    uint64_t h[24 * 14];
+    PPL_CUDA(L, cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, L->stream));
+    PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+    const uint64_t t0 = h[0];
+    for (int t = 0; t < 24; ++t) {
+      fprintf(stderr, "ts tile %2d:", t);
+      for (int s = 0; s < 14; ++s)
+        fprintf(stderr, " %7.2f", h[t * 14 + s] ? (double)(int64_t)(h[t * 14 + s] - t0) / 1e3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   L->last_was_gather = false;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));

@@ -63,6 +63,7 @@ def test_fused_linear_matches_oracle(pp, F, D, zdt):
         Z = torch.full((3, B, H, D), float("nan"), dtype=tdt, device="cuda")
         t = 0
         while t < steps:
+            Z.fill_(float("nan"))
             rows = L.next_batches_linear(3, Wd, D, Z, zdt, B * H * D * esz)
             torch.cuda.synchronize()
             for i, nr in enumerate(rows):
