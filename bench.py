@@ -313,6 +313,8 @@ def run_ours(args):
     L.close()
     torch.cuda.empty_cache()
 
+    if W == 1 and name == "products" and not args.skip_consumer:
+        result["consumer_fused_linear"] = consumer_fused_linear(pp, torch, cfg, args)
     if W == 1 and not args.skip_e2e:
         result["e2e"] = e2e_host_store(pp, torch, cfg, args)
     if rank == 0 and W == 1 and not args.skip_cpu:
@@ -327,6 +329,56 @@ def run_ours(args):
         print(json.dumps(result))
     if dist:
         dist.destroy_process_group()
+
+
+def consumer_fused_linear(pp, torch, cfg, args, D=512, k=8, reps=5):
+    """§8(f)-1: the batch consumed by SIGN's per-hop linear layer (hidden 512) in
+    the fused tcgen05 kernel (pp_next_batches_linear) -- epochs of permutation + fused
+    gather/cast/GEMM, the batch never written to HBM.  Bound: HBM (1600 B read + 4096 B of bf16 Z
+    written per node); the tensor work is 2*H*F*D = 410 kFLOP per node."""
+    import numpy as np
+
+    N, H, F, B = cfg["N"], cfg["H"], cfg["F"], cfg["B"]
+    L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16)
+    L.fill_synthetic(DATA_SEED)
+    st = torch.cuda.Stream()
+    L.set_stream(st)
+    steps = L.query()["steps_per_epoch"]
+    W = torch.from_numpy((np.random.default_rng(0).standard_normal((H, F, D)) / 10).astype(np.float32)).cuda()
+    W = W.to(torch.bfloat16)
+    nslots = 16
+    Z = torch.empty((nslots, B, H, D), dtype=torch.bfloat16, device="cuda")
+    zs = B * H * D * 2
+
+    def epoch(e):
+        L.epoch_permute(SEED0 + e, cfg["chunk"], st)
+        L.epoch_prefetch(SEED0 + e + 1, cfg["chunk"])
+        done = 0
+        while done < steps:
+            s0 = done % nslots
+            done += len(L.next_batches_linear(min(k, steps - done, nslots - s0), W, D, Z[s0], "bf16", zs, st))
+
+    with torch.cuda.stream(st):
+        epoch(0)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        a.record(st)
+        for i in range(reps):
+            epoch(1 + i)
+        b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    L.close()
+    del Z
+    torch.cuda.empty_cache()
+    peak, _ = peaks()
+    per_node = H * F * 4 + H * D * 2 + 4
+    return {"value": N / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "hidden": D,
+            "achieved_GBs": N * per_node / ms / 1e6, "frac_hbm": N * per_node / ms / 1e6 / peak,
+            "tflops": 2.0 * N * H * F * D / ms / 1e9,
+            "note": "fused gather + cast + per-hop linear (tcgen05, TMEM accumulators); "
+                    "unfused loader + cuBLAS reference: profiles/r1e_bench_fused_linear.jsonl"}
 
 
 def e2e_host_store(pp, torch, cfg, args):
@@ -384,6 +436,7 @@ def main():
     ap.add_argument("--prefetch", type=int, default=1, help="overlap the next epoch's permutation (1/0)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-consumer", action="store_true", help="skip the §8(f)-1 fused-linear measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
