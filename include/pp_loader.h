@@ -202,6 +202,23 @@ pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride
 pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,
                                  int64_t z_stride_bytes, int32_t* rows, int32_t* n_done, void* consumer_stream);
 
+/* Pre-propagation on the GPU (Eq. (2)):
+ * hops[k] = B hops[k-1] for k = 1..K, hops[0] = X, with the SGC/SIGN/HOGA
+ * operator B = D~^{-1/2} (I + A) D~^{-1/2}.
+ *   row_ptr: device int64 [n+1], col_idx: device int64 [nnz] -- CSR of
+ *            A~ = I + A: symmetric, exactly one diagonal entry per row,
+ *            columns ascending within a row (d~_i = row length).
+ *   X:    device fp32 [n][F] row-major; hops: device fp32 [K+1][n][F].
+ * Arithmetic: w_ij = 1/sqrt(d~_i d~_j) in fp64, row sums in ascending column
+ * order in fp64 with separately rounded products and sums, one RNE rounding
+ * to fp32 per output (bit-identical to the CPU reference definition).
+ * Enqueued on `stream`; temporary fp64 weights (8 B per nonzero) are
+ * allocated stream-ordered.  Reads row_ptr[n] synchronously.
+ * Errors: PP_ERR_INVALID (n < 1, F not in [1, 256], K < 0, NULL pointers),
+ * PP_ERR_OOM, PP_ERR_CUDA. */
+pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col_idx, const float* X,
+                       int32_t K, float* hops, void* stream);
+
 /* Move the cursor to step t (0 <= t <= steps_per_epoch): resume support.
  * (seed, chunk, cursor) is the loader's whole epoch state. */
 pp_status pp_seek(pp_loader* L, int64_t step);

@@ -26,7 +26,7 @@ __all__ = [
     "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_epoch_prefetch", "pp_next_batch", "pp_next_batches",
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
-    "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear",
+    "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
 ]
 
 
@@ -162,6 +162,14 @@ def pp_next_batches_linear(h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stre
                                       ctypes.byref(done), _stream(consumer_stream))
     _check(rc, "pp_next_batches_linear", ok=(PP_OK, PP_END_OF_EPOCH))
     return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
+
+
+def pp_propagate(row_ptr, col_idx, X, K, hops, stream=None) -> None:
+    """Eq. (2) on the GPU: hops[k] = B hops[k-1], hops[0] = X (device tensors: int64 CSR of I + A,
+    fp32 X [n, F], fp32 hops [K+1, n, F])."""
+    n, F = X.shape
+    _check(lib().pp_propagate(n, F, _ptr(row_ptr), _ptr(col_idx), _ptr(X), K, _ptr(hops), _stream(stream)),
+           "pp_propagate")
 
 
 def pp_seek(h, step: int) -> None:

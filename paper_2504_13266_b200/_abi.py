@@ -18,7 +18,7 @@ EXPORTS = [
     "pp_loader_create", "pp_loader_destroy", "pp_epoch_permute", "pp_epoch_prefetch", "pp_next_batch", "pp_next_batches", "pp_seek",
     "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
-    "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear",
+    "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
 ]
 
 
@@ -110,6 +110,7 @@ def lib():
                 "pp_read_store": (st, [P, i64, i64, P]),
                 "pp_debug_set_sort_bits_delta": (st, [P, i32]),
                 "pp_next_batches_linear": (st, [P, i32, P, i32, P, ctypes.c_int, i64, P, P, P]),
+                "pp_propagate": (st, [i64, i32, P, P, P, i32, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

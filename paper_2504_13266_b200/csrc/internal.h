@@ -94,6 +94,12 @@ struct LinearArgs {
 bool linear_supported(int H, int F, int D, int num_sms);
 cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st);
 
+// ---- Eq. (2) propagation (propagate.cu) --------------------------------------
+cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int64_t* col, double* val,
+                                   cudaStream_t st);
+cudaError_t launch_spmm(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col, const double* val,
+                        const float* x, float* y, cudaStream_t st);
+
 // ---- synthetic fill (gather.cu) ---------------------------------------------
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
                                   int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,

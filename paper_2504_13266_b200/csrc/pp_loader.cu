@@ -236,6 +236,42 @@ int32_t pp_abi_version(void) { return PP_ABI_VERSION; }
 
 const char* pp_last_error(void) { return g_last_error.c_str(); }
 
+pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col_idx, const float* X,
+                       int32_t K, float* hops, void* stream) {
+  if (n < 1 || F < 1 || F > 256 || K < 0) return fail(PP_ERR_INVALID, "need n >= 1, 1 <= F <= 256, K >= 0");
+  if (!row_ptr || !col_idx || !X || !hops) return fail(PP_ERR_INVALID, "NULL pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t nnz = 0;
+  cudaError_t e = cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(PP_ERR_CUDA, "reading row_ptr[n]: %s", cudaGetErrorString(e));
+  if (nnz < n) return fail(PP_ERR_INVALID, "row_ptr[n] = %lld < n: every row needs its diagonal entry", (long long)nnz);
+  const size_t plane = static_cast<size_t>(n) * F * sizeof(float);
+  e = cudaMemcpyAsync(hops, X, plane, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return fail(PP_ERR_CUDA, "hop 0 copy: %s", cudaGetErrorString(e));
+  if (K == 0) return PP_OK;
+  double* val = nullptr;
+  {  // keep the stream-ordered pool's memory between calls (the default threshold unmaps it at every sync)
+    static bool pool_set = false;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (!pool_set && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pool_set = true;
+    }
+  }
+  if (cudaMallocAsync(reinterpret_cast<void**>(&val), static_cast<size_t>(nnz) * sizeof(double), st) != cudaSuccess)
+    return fail(PP_ERR_OOM, "operator values (%lld nonzeros)", (long long)nnz);
+  e = launch_operator_values(n, row_ptr, col_idx, val, st);
+  for (int32_t k = 1; k <= K && e == cudaSuccess; ++k)
+    e = launch_spmm(n, F, row_ptr, col_idx, val, hops + (k - 1) * (plane / sizeof(float)),
+                    hops + k * (plane / sizeof(float)), st);
+  cudaFreeAsync(val, st);
+  if (e != cudaSuccess) return fail(PP_ERR_CUDA, "propagation: %s", cudaGetErrorString(e));
+  return PP_OK;
+}
+
 int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_bytes_, int32_t num_ops,
                            int32_t num_hops_R) {
   if (num_nodes < 0 || feat_dim < 0 || elem_bytes_ < 0 || num_ops < 0 || num_hops_R < 0) return -1;

@@ -1,0 +1,54 @@
+"""§8(f)-2 measurement: pp_propagate (Eq. (2), K = 3 hops) on an ogbn-products-sized synthetic
+undirected graph (n = 2,449,029 nodes, 61,859,140 drawn edges -> ~126 M nonzeros of I + A after
+symmetrising and dedup, F = 100).  The CSR is built on the GPU with torch (input preparation);
+the timed region is pp_propagate only.  One JSON line."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import __graft_entry__ as ge  # noqa: E402
+
+ge.build()
+import paper_2504_13266_b200 as pp  # noqa: E402
+
+n, m, F, K = 2_449_029, 61_859_140, 100, 3
+g = torch.Generator(device="cuda").manual_seed(2504)
+src = torch.randint(0, n, (m,), device="cuda", generator=g)
+dst = torch.randint(0, n, (m,), device="cuda", generator=g)
+keep = src != dst
+src, dst = src[keep], dst[keep]
+diag = torch.arange(n, device="cuda")
+keys = torch.cat([src * n + dst, dst * n + src, diag * n + diag])
+del src, dst, keep
+keys = torch.unique(keys)  # sorted: rows ascending, columns ascending within a row
+rows = keys // n
+col = (keys % n).contiguous()
+del keys
+row_ptr = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+row_ptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
+del rows
+nnz = int(row_ptr[-1])
+X = torch.randn((n, F), device="cuda", generator=g)
+hops = torch.empty((K + 1, n, F), device="cuda")
+torch.cuda.synchronize()
+pp.pp_propagate(row_ptr, col, X, K, hops)  # warm-up
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+reps = 3
+a.record()
+for _ in range(reps):
+    pp.pp_propagate(row_ptr, col, X, K, hops)
+b.record()
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / reps
+# algorithmic bytes: per hop every nonzero reads its neighbour row (F*4) + column (8) + weight (8),
+# every row writes F*4 and reads 2 row pointers; plus the weights pass and the hop-0 copy
+per_hop = nnz * (F * 4 + 16) + n * (F * 4 + 16)
+total = K * per_hop + nnz * (8 + 8 + 16) + 2 * n * F * 4
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
+print(json.dumps({"config": "products-sized ER graph", "n": n, "nnz": nnz, "F": F, "K": K, "ms": ms,
+                  "algorithmic_GBs": total / ms / 1e6, "frac_hbm": total / ms / 1e6 / peak,
+                  "ms_per_hop": ms / K}))
