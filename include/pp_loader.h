@@ -127,6 +127,8 @@ typedef struct {
   int64_t cursor;           /* next step index */
   int32_t permuted;         /* 1 after the first pp_epoch_permute */
   int32_t gather_path;      /* 0 = vector (16-B) path, 1 = scalar fallback */
+  int32_t local_epoch;      /* 1 if the current epoch came from pp_epoch_permute_local */
+  int64_t epoch_positions;  /* positions of the current epoch (N, or local_rows when local) */
 } pp_loader_info;
 
 /* Create a loader.  Copies the hop data into a library-owned, node-major store
@@ -147,6 +149,17 @@ pp_status pp_loader_destroy(pp_loader* L);
  * Collective for W > 1: every rank passes the same (seed, chunk).
  * Errors: PP_ERR_INVALID (chunk out of range), PP_ERR_CUDA. */
 pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream);
+
+/* Locality-aware alternative for sharded loaders ("data
+ * loader fetching data in a locality-aware manner"): this rank
+ * shuffles only the local_rows nodes it owns (local row lr = global node
+ * lr*W + rank), with the same Philox argsort and chunk rules over local
+ * positions, and its batches are slices [tB, min((t+1)B, local_rows)) of that
+ * order -- every row comes from local HBM, no peer traffic.  Not collective;
+ * results depend on W (each rank sees only its shard).  Requires no node set.
+ * steps_per_epoch (pp_loader_query) becomes ceil(local_rows / B) until the
+ * next pp_epoch_permute.  Errors: PP_ERR_INVALID (chunk, node set), PP_ERR_CUDA. */
+pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, void* stream);
 
 /* Compute the order of a FUTURE epoch now, on a library side stream, so that
  * it overlaps the current epoch's batches (the per-epoch shuffle runs "at the

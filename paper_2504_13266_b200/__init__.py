@@ -27,6 +27,7 @@ __all__ = [
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
     "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
+    "pp_epoch_permute_local",
 ]
 
 
@@ -131,6 +132,11 @@ def pp_epoch_permute(h, seed: int, chunk: int = 1, stream=None) -> None:
     _check(lib().pp_epoch_permute(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk, _stream(stream)), "pp_epoch_permute")
 
 
+def pp_epoch_permute_local(h, seed: int, chunk: int = 1, stream=None) -> None:
+    _check(lib().pp_epoch_permute_local(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk, _stream(stream)),
+           "pp_epoch_permute_local")
+
+
 def pp_epoch_prefetch(h, seed: int, chunk: int = 1) -> None:
     _check(lib().pp_epoch_prefetch(h, ctypes.c_uint64(seed & (2**64 - 1)), chunk), "pp_epoch_prefetch")
 
@@ -191,7 +197,7 @@ def pp_fill_synthetic(h, data_seed: int) -> None:
 
 
 def pp_get_order(h) -> np.ndarray:
-    n = pp_loader_query(h)["num_positions"]
+    n = pp_loader_query(h)["epoch_positions"]
     out = np.zeros(n, dtype=np.int64)
     _check(lib().pp_get_order(h, out.ctypes.data), "pp_get_order")
     return out
@@ -250,6 +256,9 @@ class Loader:
 
     def epoch_permute(self, seed, chunk=1, stream=None):
         pp_epoch_permute(self.h, seed, chunk, stream)
+
+    def epoch_permute_local(self, seed, chunk=1, stream=None):
+        pp_epoch_permute_local(self.h, seed, chunk, stream)
 
     def epoch_prefetch(self, seed, chunk=1):
         pp_epoch_prefetch(self.h, seed, chunk)

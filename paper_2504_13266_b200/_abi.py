@@ -19,6 +19,7 @@ EXPORTS = [
     "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
     "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
+    "pp_epoch_permute_local",
 ]
 
 
@@ -72,6 +73,8 @@ class pp_loader_info(ctypes.Structure):
         ("cursor", ctypes.c_int64),
         ("permuted", ctypes.c_int32),
         ("gather_path", ctypes.c_int32),
+        ("local_epoch", ctypes.c_int32),
+        ("epoch_positions", ctypes.c_int64),
     ]
 
 
@@ -111,6 +114,7 @@ def lib():
                 "pp_debug_set_sort_bits_delta": (st, [P, i32]),
                 "pp_next_batches_linear": (st, [P, i32, P, i32, P, ctypes.c_int, i64, P, P, P]),
                 "pp_propagate": (st, [i64, i32, P, P, P, i32, P, P]),
+                "pp_epoch_permute_local": (st, [P, u64, i64, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -26,7 +26,16 @@ struct SortScratch {
   uint32_t* tmp;        // [U]       unit ids grouped by bucket
   uint32_t* ragged;     // [1]       position of the ragged chunk in pi
   uint32_t k32_mask = 0xffffffffu;  // test knob: compare fewer sub-key bits (forces the tie path)
+  uint32_t* hist = nullptr;  // two-level path: per-tile digit counts, then offsets
+  size_t hist_cap = 0;       // entries allocated in hist
+  uint32_t l2_cap = 0xffffffffu;  // test knob (PPLOAD_DEBUG_L2CAP): smaller level-2 capacity forces the fallback
+  // Two-level radix path (PPLOAD_PERMUTE=two_level): no global atomics, but measured
+  // slower than the bucket sort on products (124 vs 111 us, and it interferes more
+  // with overlapped gathers, profiles/r1g_*), so off by default.
+  bool two_level = false;
 };
+// Entries of SortScratch::hist the two-level path needs for U units (0: path not used).
+size_t two_level_hist_entries(uint64_t U);
 constexpr int kScanTile = 4096;
 
 // Buckets used for U units: 2^bits with U / 2^bits in ~[14, 28).
@@ -41,6 +50,9 @@ cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool al
 // order[p], p in [0, N): chunk expansion of pi (chunk c, U = ceil(N / c)).
 cudaError_t launch_chunk_expand(const uint32_t* pi, uint32_t U, uint64_t N, uint64_t c, const uint32_t* ragged,
                                 uint32_t* order, cudaStream_t st);
+
+// Local shuffle (pp_epoch_permute_local): order[p] <- order[p] * W + r.
+cudaError_t launch_local_to_global(uint32_t* order, int64_t n, int32_t W, int32_t r, cudaStream_t st);
 
 // ---- batch assembly (gather.cu) ----------------------------------------------
 struct GatherArgs {

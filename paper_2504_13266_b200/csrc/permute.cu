@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(uint32_t* __restrict
   for (int q = 0; q < 4; ++q) {
     if (i0 + q < n) {
       counts[i0 + q] = v[q] + off;
-      if (i0 + q + 1 < n) cursor[i0 + q] = v[q] + off;
+      if (cursor != nullptr && i0 + q + 1 < n) cursor[i0 + q] = v[q] + off;
     }
   }
 }
@@ -269,10 +269,186 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cta_sort(uint64_t seed, uin
   }
 }
 
+// Local shuffle: local row lr -> global node lr * W + r, in place.
+__global__ void k_local_to_global(uint32_t* __restrict__ order, int64_t n, uint32_t W, uint32_t r) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    order[p] = order[p] * W + r;
+}
+
+cudaError_t launch_local_to_global(uint32_t* order, int64_t n, int32_t W, int32_t r, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_local_to_global<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(order, n, W, r);
+  return cudaGetLastError();
+}
+
 // Position of the ragged (last) chunk U-1 inside pi.
 __global__ void k_find_ragged(const uint32_t* __restrict__ pi, uint32_t U, uint32_t* __restrict__ ragged) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x)
     if (pi[i] == U - 1) *ragged = i;
+}
+
+// ---- two-level radix path (4096 < U <= 2^23): no global atomics -------------
+// Level 1: CTA tiles of kL1Tile units histogram the top b1 key bits in shared
+// memory; a digit-major scan of the per-tile counts gives every tile its own
+// output offsets, so the scatter needs only shared-memory atomics.  Level 2:
+// one CTA per level-1 bucket (~1-2 K units) reloads its units, counting-sorts
+// them in shared memory by the next b2 bits into sub-buckets of ~8, and ranks
+// each unit inside its sub-bucket by full (key, id).  The order produced by
+// the atomics never shows: every rank is unique.
+constexpr uint32_t kL1Tile = 8192;
+constexpr int kL1Threads = 512;
+constexpr int kL2Threads = 256;
+constexpr uint32_t kL2Cap = 2048;         // units of one level-1 bucket held in shared memory
+constexpr uint32_t kTwoLevelMaxU = 1u << 22;  // b1 <= 12 keeps the mean bucket <= 1024 (cap = mean + 32 sigma)
+
+struct TwoLevel {
+  int b1, b2;
+  uint32_t ntiles;
+};
+static TwoLevel two_level_shape(uint32_t U) {
+  TwoLevel t{};
+  int b1 = 1;
+  while (b1 < 12 && (U >> b1) > 1024) ++b1;  // mean level-1 bucket <= 1024 units
+  const uint32_t mean = U >> b1;
+  int b2 = 0;
+  while (b2 < 10 && (mean >> (b2 + 1)) >= 8) ++b2;  // sub-buckets of ~8-16 units
+  t.b1 = b1;
+  t.b2 = b2;
+  t.ntiles = (U + kL1Tile - 1) / kL1Tile;
+  return t;
+}
+
+size_t two_level_hist_entries(uint64_t U) {
+  if (U <= kCtaSortMax || U > kTwoLevelMaxU) return 0;
+  const TwoLevel t = two_level_shape(static_cast<uint32_t>(U));
+  return (static_cast<size_t>(1) << t.b1) * t.ntiles + 1;
+}
+
+__global__ void __launch_bounds__(kL1Threads) k_l1_hist(uint64_t seed, uint32_t U, int b1, uint32_t ntiles,
+                                                         uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t s_hist[];
+  const uint32_t nd = 1u << b1;
+  for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) s_hist[d] = 0;
+  __syncthreads();
+  const uint32_t u0 = blockIdx.x * kL1Tile;
+  for (uint32_t u = u0 + threadIdx.x; u < min(U, u0 + kL1Tile); u += blockDim.x)
+    atomicAdd(&s_hist[static_cast<uint32_t>(unit_sort_key(seed, u) >> (64 - b1))], 1u);
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) hist[d * ntiles + blockIdx.x] = s_hist[d];
+}
+
+__global__ void __launch_bounds__(kL1Threads) k_l1_scatter(uint64_t seed, uint32_t U, int b1, uint32_t ntiles,
+                                                            const uint32_t* __restrict__ offs,
+                                                            uint32_t* __restrict__ tmp) {
+  extern __shared__ uint32_t s_cur[];
+  const uint32_t nd = 1u << b1;
+  for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) s_cur[d] = offs[d * ntiles + blockIdx.x];
+  __syncthreads();
+  const uint32_t u0 = blockIdx.x * kL1Tile;
+  for (uint32_t u = u0 + threadIdx.x; u < min(U, u0 + kL1Tile); u += blockDim.x) {
+    const uint32_t slot = atomicAdd(&s_cur[static_cast<uint32_t>(unit_sort_key(seed, u) >> (64 - b1))], 1u);
+    tmp[slot] = u;
+  }
+}
+
+// One CTA per level-1 bucket.  Buckets larger than kL2Cap (a > 40-sigma event
+// for the chosen means) fall back to a warp ranking straight from global memory.
+__global__ void __launch_bounds__(kL2Threads) k_l2_sort(uint64_t seed, int b1, int b2, uint32_t ntiles, uint32_t U,
+                                                         uint32_t cap,
+                                                         const uint32_t* __restrict__ offs,
+                                                         const uint32_t* __restrict__ tmp, uint32_t* __restrict__ pi) {
+  __shared__ uint64_t s_key[kL2Cap];
+  __shared__ uint32_t s_u[kL2Cap];
+  __shared__ uint16_t s_perm[kL2Cap];
+  __shared__ uint32_t s_cnt[1025], s_off[1025];
+  const uint32_t d = blockIdx.x, nd = 1u << b1;
+  const uint32_t beg = offs[d * ntiles];
+  const uint32_t end = d + 1 < nd ? offs[(d + 1) * ntiles] : U;
+  const uint32_t n = end - beg;
+  if (n == 0) return;
+  if (n > cap) {  // generic fallback: warp 0 ranks by full (key, id), tiles of 32 x 32
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    for (uint32_t ibase = 0; ibase < n; ibase += 32) {
+      const bool vi = ibase + lane < n;
+      const uint32_t ui = vi ? tmp[beg + ibase + lane] : 0xffffffffu;
+      const uint64_t ki = vi ? unit_sort_key(seed, ui) : ~0ull;
+      uint32_t rank = 0;
+      for (uint32_t jbase = 0; jbase < n; jbase += 32) {
+        const bool vj = jbase + lane < n;
+        const uint32_t uj = vj ? tmp[beg + jbase + lane] : 0xffffffffu;
+        const uint64_t kj = vj ? unit_sort_key(seed, uj) : ~0ull;
+        const uint32_t m = min(32u, n - jbase);
+        for (uint32_t s = 0; s < m; ++s) {
+          const uint64_t kk = __shfl_sync(0xffffffffu, kj, s);
+          const uint32_t uu = __shfl_sync(0xffffffffu, uj, s);
+          rank += (kk < ki) | ((kk == ki) & (uu < ui));
+        }
+      }
+      if (vi) pi[beg + rank] = ui;
+    }
+    return;
+  }
+  const uint32_t ns = 1u << b2;
+  for (uint32_t s = threadIdx.x; s <= ns; s += blockDim.x) s_cnt[s] = 0;
+  __syncthreads();
+  const int shift = 64 - b1 - b2;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t u = tmp[beg + i];
+    const uint64_t key = unit_sort_key(seed, u);
+    s_key[i] = key;
+    s_u[i] = u;
+    atomicAdd(&s_cnt[b2 ? static_cast<uint32_t>((key << b1) >> (64 - b2)) : 0u], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan of <= 1024 sub-bucket counts
+    uint32_t acc = 0;
+    for (uint32_t s = 0; s < ns; ++s) {
+      s_off[s] = acc;
+      acc += s_cnt[s];
+      s_cnt[s] = s_off[s];  // reuse as scatter cursor
+    }
+    s_off[ns] = acc;
+  }
+  __syncthreads();
+  (void)shift;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t sb = b2 ? static_cast<uint32_t>((s_key[i] << b1) >> (64 - b2)) : 0u;
+    s_perm[atomicAdd(&s_cnt[sb], 1u)] = static_cast<uint16_t>(i);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t ki = s_key[i];
+    const uint32_t ui = s_u[i];
+    const uint32_t sb = b2 ? static_cast<uint32_t>((ki << b1) >> (64 - b2)) : 0u;
+    const uint32_t lo = s_off[sb], hi = s_off[sb + 1];
+    uint32_t rank = 0;
+    for (uint32_t p = lo; p < hi; ++p) {
+      const uint32_t j = s_perm[p];
+      const uint64_t kj = s_key[j];
+      rank += (kj < ki) | ((kj == ki) & (s_u[j] < ui));
+    }
+    pi[beg + lo + rank] = ui;
+  }
+}
+
+static cudaError_t launch_two_level(uint64_t seed, uint32_t U, const SortScratch& s, uint32_t* pi,
+                                    cudaStream_t st) {
+  const TwoLevel t = two_level_shape(U);
+  const uint32_t nd = 1u << t.b1;
+  const uint32_t n = nd * t.ntiles + 1;  // hist[n-1] = 0 -> offs[n-1] = U
+  cudaError_t e = cudaMemsetAsync(s.hist + (n - 1), 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  k_l1_hist<<<t.ntiles, kL1Threads, nd * 4, st>>>(seed, U, t.b1, t.ntiles, s.hist);
+  const uint32_t nblk = (n + kScanTile - 1) / kScanTile;
+  k_scan_reduce<<<nblk, kScanThreads, 0, st>>>(s.hist, n, s.blocksums);
+  k_scan_top<<<1, kScanThreads, 0, st>>>(s.blocksums, nblk);
+  k_scan_down<<<nblk, kScanThreads, 0, st>>>(s.hist, n, s.blocksums, nullptr);
+  k_l1_scatter<<<t.ntiles, kL1Threads, nd * 4, st>>>(seed, U, t.b1, t.ntiles, s.hist, s.tmp);
+  k_l2_sort<<<nd, kL2Threads, 0, st>>>(seed, t.b1, t.b2, t.ntiles, U, std::min(kL2Cap, s.l2_cap), s.hist, s.tmp,
+                                       pi);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool allow_cta, const SortScratch& s, uint32_t* pi,
@@ -283,6 +459,13 @@ cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool al
     while (P < U) P <<= 1;
     k_cta_sort<<<1, kCtaSortThreads, P * 12, st>>>(seed, U, P, pi, ragged);
     return cudaGetLastError();
+  }
+  if (allow_cta && s.two_level && s.hist != nullptr && two_level_hist_entries(U) != 0 &&
+      two_level_hist_entries(U) <= s.hist_cap) {
+    cudaError_t e = launch_two_level(seed, U, s, pi, st);
+    if (e == cudaSuccess && ragged != nullptr)
+      k_find_ragged<<<std::min<uint32_t>((U + 255) / 256, 148u * 8u), 256, 0, st>>>(pi, U, ragged);
+    return e == cudaSuccess ? cudaGetLastError() : e;
   }
   const uint32_t nb = 1u << bits;
   const uint32_t n = nb + 1;  // counts[nb] = 0 -> offsets[nb] = U

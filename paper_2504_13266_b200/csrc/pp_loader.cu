@@ -101,6 +101,8 @@ struct pp_loader {
   std::vector<void*> ipc_opened;
 
   bool permuted = false, poisoned = false;
+  bool local = false;         // current epoch from pp_epoch_permute_local
+  int64_t steps_global = 0;   // steps of a global-permutation epoch
   uint64_t seed = 0;
   int64_t chunk = 1, cursor = 0;
 };
@@ -135,6 +137,7 @@ void release(pp_loader* L) {
   cudaFree(L->sort.blocksums);
   cudaFree(L->sort.tmp);
   cudaFree(L->sort.ragged);
+  cudaFree(L->sort.hist);
   if (L->ev_in) cudaEventDestroy(L->ev_in);
   if (L->ev_out) cudaEventDestroy(L->ev_out);
   if (L->ev_pref) cudaEventDestroy(L->ev_pref);
@@ -211,20 +214,25 @@ pp_status validate(const pp_loader_desc* d) {
 }
 
 pp_status ensure_sort_scratch(pp_loader* L, uint32_t U, int bits) {
-  if (bits > L->sort_bits_max || !L->sort.counts) {
+  const size_t hist_need = L->sort.two_level ? two_level_hist_entries(U) : 0;
+  if (bits > L->sort_bits_max || !L->sort.counts || hist_need > L->sort.hist_cap) {
     const int nbits = std::max(bits, L->sort_bits_max);
+    const size_t hist_cap = std::max(hist_need, L->sort.hist_cap);
     cudaFree(L->sort.counts);
     cudaFree(L->sort.cursor);
     cudaFree(L->sort.blocksums);
-    L->sort.counts = L->sort.cursor = L->sort.blocksums = nullptr;
+    cudaFree(L->sort.hist);
+    L->sort.counts = L->sort.cursor = L->sort.blocksums = L->sort.hist = nullptr;
+    L->sort.hist_cap = 0;
     const size_t nb = size_t(1) << nbits;
-    const size_t nblk = (nb + 1 + kScanTile - 1) / kScanTile;
+    const size_t nblk = (std::max(nb + 1, hist_cap) + kScanTile - 1) / kScanTile;  // scans of either path
     if (cudaMalloc(&L->sort.counts, (nb + 1) * 4) != cudaSuccess || cudaMalloc(&L->sort.cursor, nb * 4) != cudaSuccess ||
-        cudaMalloc(&L->sort.blocksums, nblk * 4) != cudaSuccess)
+        cudaMalloc(&L->sort.blocksums, nblk * 4) != cudaSuccess ||
+        (hist_cap > 0 && cudaMalloc(&L->sort.hist, hist_cap * 4) != cudaSuccess))
       return fail(PP_ERR_OOM, "sort scratch allocation failed (2^%d buckets)", nbits);
     L->sort_bits_max = nbits;
+    L->sort.hist_cap = hist_cap;
   }
-  (void)U;
   return PP_OK;
 }
 
@@ -305,6 +313,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   L->B = desc->batch_size;
   const int64_t per_step = L->B * L->W;
   L->steps = desc->drop_last ? L->N / per_step : (L->N + per_step - 1) / per_step;
+  L->steps_global = L->steps;
   L->local_rows = (L->N_total - L->rank + L->W - 1) / L->W;
   L->rec_in = static_cast<int64_t>(L->HF) * elem_bytes(L->in_dtype);
   L->rec_stride = (L->rec_in + 15) / 16 * 16;
@@ -380,6 +389,8 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     const int n = std::max(1, std::min(32, atoi(e)));
     L->sort.k32_mask = n == 32 ? 0xffffffffu : ~((1u << (32 - n)) - 1u);
   }
+  if (const char* e = getenv("PPLOAD_DEBUG_L2CAP")) L->sort.l2_cap = static_cast<uint32_t>(std::max(1, atoi(e)));
+  if (const char* e = getenv("PPLOAD_PERMUTE")) L->sort.two_level = !strcmp(e, "two_level");
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
@@ -414,8 +425,10 @@ pp_status pp_debug_set_sort_bits_delta(pp_loader* L, int32_t delta) {
   return PP_OK;
 }
 
-static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint32_t* order, cudaStream_t st) {
-  const uint32_t U = static_cast<uint32_t>((L->N + chunk - 1) / chunk);
+// order[0..n) = the epoch order of n positions for (seed, chunk) (oracle O5-O7).
+static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint32_t* order, cudaStream_t st,
+                               int64_t n) {
+  const uint32_t U = static_cast<uint32_t>((n + chunk - 1) / chunk);
   const int bits = sort_bucket_bits(U, L->sort_bits_delta);
   pp_status ps = ensure_sort_scratch(L, U, bits);
   if (ps != PP_OK) return ps;
@@ -429,9 +442,46 @@ static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint3
       L->pi_cap = U;
     }
     PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort_bits_delta == 0, L->sort, L->d_pi, L->sort.ragged, st));
-    PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(L->N), static_cast<uint64_t>(chunk),
+    PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(n), static_cast<uint64_t>(chunk),
                                     L->sort.ragged, order, st));
   }
+  return PP_OK;
+}
+
+// SURVEY.md §8(f)-4, the paper's "locality-aware" placement taken
+// literally: each rank shuffles only the rows it owns, so every batch is read
+// from local HBM and no exchange is needed at any W.  Local position lr maps
+// to global node lr * W + rank.  Not collective; ranks may use different seeds.
+pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, void* stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (L->d_node_set) return fail(PP_ERR_INVALID, "local shuffling is defined without a node set");
+  if (chunk < 1 || chunk > L->local_rows)
+    return fail(PP_ERR_INVALID, "chunk must be in [1, local_rows=%lld]", (long long)L->local_rows);
+  DevGuard g(L->dev);
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  if (user != L->stream) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, user));
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+  }
+  if (L->pref_pending) {  // a pending (global) prefetch shares the scratch: order after it, discard it
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_pref, 0));
+    L->pref_pending = false;
+  }
+  pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream, L->local_rows);
+  if (ps != PP_OK) return ps;
+  if (L->W > 1) PPL_CUDA(L, launch_local_to_global(L->d_order, L->local_rows, L->W, L->rank, L->stream));
+  if (user != L->stream) {
+    PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+    PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
+  }
+  L->local = true;
+  L->steps = L->desc.drop_last ? L->local_rows / L->B : (L->local_rows + L->B - 1) / L->B;
+  L->last_was_gather = false;
+  L->permuted = true;
+  L->seed = seed;
+  L->chunk = chunk;
+  L->cursor = 0;
   return PP_OK;
 }
 
@@ -453,17 +503,19 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
       L->cur ^= 1;  // the prefetched order becomes current
       L->d_order = L->d_orders[L->cur];
     } else {
-      pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream);
+      pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream, L->N);
       if (ps != PP_OK) return ps;
     }
   } else {
-    pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream);
+    pp_status ps = enqueue_order(L, seed, chunk, L->d_order, L->stream, L->N);
     if (ps != PP_OK) return ps;
   }
   if (user != L->stream) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
   }
+  L->local = false;
+  L->steps = L->steps_global;
   L->last_was_gather = false;
   L->permuted = true;
   L->seed = seed;
@@ -482,7 +534,7 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
   // the sort scratch (used by work already enqueued on the loader stream)
   PPL_CUDA(L, cudaEventRecord(L->ev_pref_in, L->stream));
   PPL_CUDA(L, cudaStreamWaitEvent(L->pstream, L->ev_pref_in, 0));
-  pp_status ps = enqueue_order(L, seed, chunk, L->d_orders[L->cur ^ 1], L->pstream);
+  pp_status ps = enqueue_order(L, seed, chunk, L->d_orders[L->cur ^ 1], L->pstream, L->N);
   if (ps != PP_OK) return ps;
   PPL_CUDA(L, cudaEventRecord(L->ev_pref, L->pstream));
   L->pref_pending = true;
@@ -497,7 +549,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1) return fail(PP_ERR_INVALID, "rows is NULL or n < 1");
   if (!L->permuted) return fail(PP_ERR_STATE, "pp_next_batch before pp_epoch_permute");
-  if (!L->linked) return fail(PP_ERR_STATE, "sharded loader: peers not linked yet");
+  if (!L->linked && !L->local) return fail(PP_ERR_STATE, "sharded loader: peers not linked yet");
   if (out_labels && !L->has_labels) return fail(PP_ERR_INVALID, "out_labels given but the loader has no labels");
   if (L->cursor >= L->steps) {
     rows[0] = 0;
@@ -522,9 +574,11 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   a.order = L->d_order;
   a.node_set = L->d_node_set;
   a.labels = L->d_labels;
-  a.N = L->N;
-  a.first_pos = L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
-  a.step_stride = L->B * L->W;
+  // global epoch: step t of rank r = positions [tWB + rB, ...) of the shared order;
+  // local epoch: step t = positions [tB, ...) of this rank's own order
+  a.N = L->local ? L->local_rows : L->N;
+  a.first_pos = L->local ? L->cursor * L->B : L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
+  a.step_stride = L->local ? L->B : L->B * L->W;
   a.B = static_cast<int32_t>(L->B);
   a.nsteps = static_cast<int32_t>(nsteps);
   a.out = static_cast<uint8_t*>(out);
@@ -555,7 +609,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   }
   for (int64_t i = 0; i < nsteps; ++i) {
     const int64_t s = a.first_pos + i * a.step_stride;
-    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - s)));
+    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - s)));
   }
   L->cursor += nsteps;
   if (n_done) *n_done = static_cast<int32_t>(nsteps);
@@ -675,6 +729,8 @@ pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
   info->cursor = L->cursor;
   info->permuted = L->permuted ? 1 : 0;
   info->gather_path = L->vector_path ? 0 : 1;
+  info->local_epoch = L->local ? 1 : 0;
+  info->epoch_positions = L->local ? L->local_rows : L->N;
   return PP_OK;
 }
 
@@ -697,9 +753,10 @@ pp_status pp_get_order(pp_loader* L, int64_t* dst_host) {
   if (!L->permuted) return fail(PP_ERR_STATE, "pp_get_order before pp_epoch_permute");
   DevGuard g(L->dev);
   int64_t* tmp = nullptr;
-  if (cudaMalloc(&tmp, L->N * 8) != cudaSuccess) return fail(PP_ERR_OOM, "order staging allocation");
-  cudaError_t e = launch_order_to_nodes(L->d_order, L->d_node_set, L->N, tmp, L->stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dst_host, tmp, L->N * 8, cudaMemcpyDeviceToHost, L->stream);
+  const int64_t n = L->local ? L->local_rows : L->N;
+  if (cudaMalloc(&tmp, n * 8) != cudaSuccess) return fail(PP_ERR_OOM, "order staging allocation");
+  cudaError_t e = launch_order_to_nodes(L->d_order, L->d_node_set, n, tmp, L->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst_host, tmp, n * 8, cudaMemcpyDeviceToHost, L->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(L, e, "pp_get_order");

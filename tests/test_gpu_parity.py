@@ -523,3 +523,16 @@ def test_order_mag240m_scale_properties(pp):
     assert (keys[1:] >= keys[:-1]).all()  # uint64 comparisons
     ties = np.nonzero(keys[1:] == keys[:-1])[0]
     assert (order[ties + 1] > order[ties]).all()
+
+
+@pytest.mark.parametrize("layout", ["hop_major", "node_major"])
+def test_device_resident_source(pp, layout):
+    # hop matrices handed over as CUDA tensors (PP_MEM_DEVICE): copied device-to-device into the store
+    H, N, F, B = 3, 2500, 40, 300
+    X, hs, rs = hop_tensor(70, H, N, F, layout)
+    Xd = torch.from_numpy(X).cuda()
+    with pp.Loader(data=Xd, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(4, 3)
+        got = run_epoch(L, B, H, F, oracle.BF16)
+        check_epoch(got, X.view(np.uint32), oracle.F32, hs, rs, H, F, oracle.epoch_order(4, N, 3), B, oracle.BF16)
