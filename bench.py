@@ -175,12 +175,18 @@ def run_ours(args):
     W = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    shared_gpu = W > ndev  # path check with several ranks per GPU (e.g. on a 1-GPU box): gloo plumbing
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if W > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = args.config or ("products" if W == 1 else "papers100M")
     cfg = dict(CONFIGS[name])
     if args.chunk is not None:
@@ -259,7 +265,7 @@ def run_ours(args):
         t = [start.elapsed_time(end), sum(b.elapsed_time(c) for _, b, c in evs),
              sum(a.elapsed_time(b) for a, b, _ in evs)]
         if dist:
-            tt = torch.tensor(t, device="cuda", dtype=torch.float64)
+            tt = torch.tensor(t, device="cpu" if shared_gpu else "cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.tolist()
         launches, done = 0, 0  # gather launches per epoch (calls never wrap the ring)
@@ -310,6 +316,9 @@ def run_ours(args):
             "ms_per_step": m1["total_ms"] / max(3, args.steps // 2), "achieved_GBs": m1["achieved"],
             "note": "one pp_next_batch call (one launch) per batch from Python; host-bound (~5.6 us per ctypes call)"}
     del ring
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()  # peers read this rank's store until every rank is done
     L.close()
     torch.cuda.empty_cache()
 
