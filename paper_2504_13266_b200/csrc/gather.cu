@@ -38,11 +38,21 @@ constexpr int kMinBlocksPerSM = 4;  // caps registers at 64 -> 32 resident warps
 enum { kF32 = 0, kBF16 = 1, kF16 = 2 };
 enum { kModeBF16 = 0, kModeF16 = 1, kModeCopy = 2 };
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
+__device__ __forceinline__ uint4 ld_stream(const void* p, int l2_prefetch = 0) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if (l2_prefetch == 2) {  // experiment knob (PPLOAD_L2_PREFETCH): 256-byte L2 prefetch hint
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  } else if (l2_prefetch == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  }
   return r;
 }
 
@@ -123,8 +133,8 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
           const uint32_t r = fast_div(e, vpr_M);
           const uint32_t c = e - r * vpr;
           const uint8_t* src = s_src[buf][r] + static_cast<int64_t>(c) * kInBytes;
-          x0[q] = ld_stream(src);
-          if (MODE != kModeCopy) x1[q] = ld_stream(src + 16);
+          x0[q] = ld_stream(src, a.l2_prefetch);
+          if (MODE != kModeCopy) x1[q] = ld_stream(src + 16, a.l2_prefetch);
         }
       }
 #pragma unroll

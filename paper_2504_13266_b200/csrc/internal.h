@@ -75,6 +75,7 @@ struct GatherArgs {
   int32_t in_dtype, out_dtype;  // pp_dtype codes
   int32_t tile_rows;        // batch rows per CTA tile (1..32)
   int32_t num_sms;
+  int32_t l2_prefetch;      // 0 none, 1 L2::128B, 2 L2::256B load hint (PPLOAD_L2_PREFETCH)
 };
 
 // One launch assembling a.nsteps steps.  pdl: launch with programmatic stream

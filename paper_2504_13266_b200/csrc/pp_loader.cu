@@ -89,11 +89,12 @@ struct pp_loader {
 
   // launch tuning (defaults; PPLOAD_TILE_ROWS / PPLOAD_PDL / PPLOAD_GRID_PER_SM override)
   int num_sms = 148;
-  int tile_rows = 16;
+  int tile_rows = 32;  // 16 vs 32 measured: 32 is ~1.4 % faster at k = 8 (profiles/r1i_exp_l2hint.jsonl)
   bool pdl = true;
   int grid_per_sm = 4;
   int gather_mode = 0;           // 0 auto, 1 ldg (register-staged), 2 tma (bulk copy); PPLOAD_GATHER
   bool tma_ok = false;
+  int l2_prefetch = 0;           // load hint experiment (PPLOAD_L2_PREFETCH)
   bool last_was_gather = false;  // previous op on the loader stream is a gather of this epoch
 
   ShardView shards[kMaxWorld]{};
@@ -391,6 +392,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   }
   if (const char* e = getenv("PPLOAD_DEBUG_L2CAP")) L->sort.l2_cap = static_cast<uint32_t>(std::max(1, atoi(e)));
   if (const char* e = getenv("PPLOAD_PERMUTE")) L->sort.two_level = !strcmp(e, "two_level");
+  if (const char* e = getenv("PPLOAD_L2_PREFETCH")) L->l2_prefetch = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
@@ -593,6 +595,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   a.out_dtype = L->out_dtype;
   a.tile_rows = L->tile_rows;
   a.num_sms = L->num_sms;
+  a.l2_prefetch = L->l2_prefetch;
   // Programmatic dependent launch only right after another gather of this epoch:
   // batches of one epoch are independent, and the first gather after a permute
   // or an event wait is fully serialised, so every gather sees a complete order.
