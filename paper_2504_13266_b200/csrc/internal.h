@@ -33,6 +33,7 @@ struct SortScratch {
   // slower than the bucket sort on products (124 vs 111 us, and it interferes more
   // with overlapped gathers, profiles/r1g_*), so off by default.
   bool two_level = false;
+  int grid_cap = 0;  // CTAs for the bucket-sort kernels (0: full grid); set for the prefetch stream
 };
 // Entries of SortScratch::hist the two-level path needs for U units (0: path not used).
 size_t two_level_hist_entries(uint64_t U);

@@ -172,9 +172,9 @@ __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32
                                                      uint32_t nb, int bits, uint32_t k32_mask,
                                                      const uint32_t* __restrict__ tmp,
                                                      uint32_t* __restrict__ pi) {
-  const uint32_t bucket = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (bucket >= nb) return;  // warp-uniform
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t bucket = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; bucket < nb; bucket += nwarps) {
   const uint32_t beg = offsets[bucket];
   const uint32_t n = offsets[bucket + 1] - beg;
   if (n <= 32) {
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32
       }
     }
     if (vi) pi[beg + rank] = ui;
-    return;
+    continue;
   }
   for (uint32_t ibase = 0; ibase < n; ibase += 32) {
     const bool vi = ibase + lane < n;
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32
     }
     if (vi) pi[beg + rank] = ui;
   }
+  }  // bucket loop
 }
 
 // K2: small unit counts (chunk reshuffling: U = ceil(N / c), e.g. 299 chunks of
@@ -472,15 +473,19 @@ cudaError_t launch_unit_permutation(uint64_t seed, uint32_t U, int bits, bool al
   cudaError_t e = cudaMemsetAsync(s.counts, 0, sizeof(uint32_t) * n, st);
   if (e != cudaSuccess) return e;
   const int threads = 256;
-  const uint32_t unit_blocks = std::min<uint32_t>((U + threads - 1) / threads, 148u * 16u);
+  // s.grid_cap > 0 (prefetch on the side stream): confine the grid-stride kernels to
+  // fewer CTAs so they leave most SMs to the concurrently running gathers
+  const uint32_t cap = s.grid_cap > 0 ? static_cast<uint32_t>(s.grid_cap) : 148u * 16u;
+  const uint32_t unit_blocks = std::min<uint32_t>((U + threads - 1) / threads, cap);
   k_hist<<<unit_blocks, threads, 0, st>>>(seed, U, bits, s.counts);
   const uint32_t nblk = (n + kScanTile - 1) / kScanTile;
   k_scan_reduce<<<nblk, kScanThreads, 0, st>>>(s.counts, n, s.blocksums);
   k_scan_top<<<1, kScanThreads, 0, st>>>(s.blocksums, nblk);
   k_scan_down<<<nblk, kScanThreads, 0, st>>>(s.counts, n, s.blocksums, s.cursor);
   k_scatter<<<unit_blocks, threads, 0, st>>>(seed, U, bits, s.cursor, s.tmp);
-  const uint64_t rank_threads = static_cast<uint64_t>(nb) * 32;
-  k_bucket_rank<<<static_cast<uint32_t>((rank_threads + 255) / 256), 256, 0, st>>>(seed, s.counts, nb, bits, s.k32_mask, s.tmp, pi);
+  const uint64_t rank_blocks = (static_cast<uint64_t>(nb) * 32 + 255) / 256;
+  k_bucket_rank<<<static_cast<uint32_t>(std::min<uint64_t>(rank_blocks, s.grid_cap > 0 ? cap : rank_blocks)), 256,
+                  0, st>>>(seed, s.counts, nb, bits, s.k32_mask, s.tmp, pi);
   if (ragged != nullptr) k_find_ragged<<<std::min<uint32_t>((U + 255) / 256, 148u * 8u), 256, 0, st>>>(pi, U, ragged);
   return cudaGetLastError();
 }

@@ -95,6 +95,10 @@ struct pp_loader {
   int gather_mode = 0;           // 0 auto, 1 ldg (register-staged), 2 tma (bulk copy); PPLOAD_GATHER
   bool tma_ok = false;
   int l2_prefetch = 0;           // load hint experiment (PPLOAD_L2_PREFETCH)
+  // CTA cap for the prefetched permutation (PPLOAD_PREFETCH_CTAS; 0 = full grid).
+  // Measured on products (profiles/r1j_exp_prefetch.jsonl): full grid 1.002 ms/epoch,
+  // 148-296 CTAs 0.972 ms, 64 CTAs 1.11-1.15 ms (the sort then outlasts the epoch).
+  int prefetch_ctas = 296;
   bool last_was_gather = false;  // previous op on the loader stream is a gather of this epoch
 
   ShardView shards[kMaxWorld]{};
@@ -393,6 +397,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   if (const char* e = getenv("PPLOAD_DEBUG_L2CAP")) L->sort.l2_cap = static_cast<uint32_t>(std::max(1, atoi(e)));
   if (const char* e = getenv("PPLOAD_PERMUTE")) L->sort.two_level = !strcmp(e, "two_level");
   if (const char* e = getenv("PPLOAD_L2_PREFETCH")) L->l2_prefetch = std::max(0, std::min(2, atoi(e)));
+  if (const char* e = getenv("PPLOAD_PREFETCH_CTAS")) L->prefetch_ctas = std::max(0, atoi(e));
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
@@ -536,7 +541,9 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
   // the sort scratch (used by work already enqueued on the loader stream)
   PPL_CUDA(L, cudaEventRecord(L->ev_pref_in, L->stream));
   PPL_CUDA(L, cudaStreamWaitEvent(L->pstream, L->ev_pref_in, 0));
+  L->sort.grid_cap = L->prefetch_ctas;  // leave most SMs to the gathers it overlaps
   pp_status ps = enqueue_order(L, seed, chunk, L->d_orders[L->cur ^ 1], L->pstream, L->N);
+  L->sort.grid_cap = 0;
   if (ps != PP_OK) return ps;
   PPL_CUDA(L, cudaEventRecord(L->ev_pref, L->pstream));
   L->pref_pending = true;
