@@ -102,7 +102,10 @@ struct LinearArgs {
   int64_t z_stride;         // bytes between step slots
   int32_t z_elem;           // 2 (bf16) or 4 (fp32)
   int32_t num_sms;
-  int32_t debug;            // experiment knob (PPLOAD_DEBUG_LINEAR): 1 skip loads, 2 skip Z stores
+  int32_t debug;            // experiment knob (PPLOAD_DEBUG_LINEAR), bits: 1 skip loads, 2 skip Z stores,
+                            // 4 skip the drain, 8 skip A-tile stores,
+                            // 64 skip MMAs, 128 no TMA stores (16-byte stores instead)
+  int32_t z_tma;            // set by launch_gather_linear: Z tensor map encoded, epilogue uses TMA stores
   uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null
 };
 bool linear_supported(int H, int F, int D, int num_sms);

@@ -22,6 +22,8 @@
 //     quadrant), fp32 -> bf16 (or fp32), 128-bit stores of Z rows.
 // HBM per batch row: H*F*4 read + H*D*s_z written (products, D = 512, bf16 Z:
 // 1600 + 4096 B) instead of 1600 + 800 (gather) + 800 + 4096 (GEMM) unfused.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -42,11 +44,11 @@ constexpr int kEpiWarp0 = 12;      // warps 12..19: TMEM lane quadrant warp % 4,
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kTileM = 128;        // batch rows per tile (UMMA M)
 constexpr int kUmmaN = 256;        // columns per accumulator (UMMA N)
-constexpr int kEpiCols = kUmmaN / (kEpiWarps / 4);  // accumulator columns drained per epilogue warp
 constexpr int kKPad = 128;         // F zero-padded to two 64-element K blocks
 constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
 constexpr int kStages = 2;
-constexpr int kStagePitch = 128;   // epilogue staging row pitch (16-byte chunks XOR-swizzled by row)
+constexpr int kStageBytes = 32 * 128;  // epilogue staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
+constexpr int kEpiBufs = 2;         // staging buffers per epilogue warp
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -135,14 +137,15 @@ __device__ __forceinline__ void dbg_ts(const LinearArgs& a, int tile, int slot, 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearArgs a) {
+__global__ void __launch_bounds__(kLinThreads, 1)
+    k_gather_linear(const LinearArgs a, const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int D = a.D;
   uint8_t* w_s = smem;                                // [2 kb][D rows][128 B]
   uint8_t* a_s = smem + 2 * D * 128;                  // [kStages][2 kb][128 rows][128 B]
-  uint8_t* z_s = a_s + kStages * kABytes;             // [8 epilogue warps][32 rows][80 B] staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * 32 * kStagePitch);
+  uint8_t* z_s = a_s + kStages * kABytes;             // [epilogue warps][kEpiBufs][32 rows][128 B] staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * kEpiBufs * kStageBytes);
   uint64_t* a_full = bars;                            // [kStages], kProducerThreads arrivals
   uint64_t* a_empty = bars + kStages;                 // [kStages], MMA commit
   uint64_t* t_full = bars + 2 * kStages;              // [2], MMA commit
@@ -224,13 +227,24 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
     // lane c = lane % 16 the K chunk 8c..8c+7 (two 16-byte fp32 loads -> one
     // 16-byte bf16 store), so no shuffles are needed to pair elements.
     const int hw = lane >> 4, c = lane & 15;
-    auto load_tile = [&](int64_t t, uint4(&x)[16]) {
+    // order[] entry of tile row rbase + lane (lanes < 16), kNoRow past the batch.
+    // Fetched one tile ahead: under the Z write stream an order[] read costs a
+    // DRAM round trip, which would otherwise precede every tile's data loads.
+    constexpr uint32_t kNoRow = 0xffffffffu;
+    auto fetch_index = [&](int64_t t) -> uint32_t {
+      if (t >= total) return kNoRow;
       int64_t step, pos;
       int r0;
       const int rows = tile_rows(t, step, r0, pos);
+      uint32_t v = kNoRow;
+      if (lane < 16 && rbase + lane < rows)
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a.order + pos + r0 + rbase + lane));
+      return v;
+    };
+    auto load_tile = [&](uint32_t idx, uint4(&x)[16]) {
       const uint8_t* my_src = nullptr;  // lane j < 16 resolves row rbase + j
-      if (lane < 16 && rbase + lane < rows) {
-        uint64_t v = a.order[pos + r0 + rbase + lane];
+      if (idx != kNoRow) {
+        uint64_t v = idx;
         if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
         my_src = a.store + static_cast<int64_t>(v) * a.rec_stride + static_cast<int64_t>(k) * F * 4;
       }
@@ -266,9 +280,14 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
     };
     uint4 x[16];
     int i = 0;
-    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
-      load_tile(t, x);
+    int64_t t = next_tile(q);
+    uint32_t idx = fetch_index(t);
+    while (t < total) {
+      const int64_t tn = next_tile(t + Q);
+      load_tile(idx, x);
+      idx = fetch_index(tn);  // in flight together with this tile's data loads
       store_tile(i++, x);
+      t = tn;
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (one lane)
@@ -289,7 +308,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
           tc_fence_after();
           if (dbg_lane) dbg_ts(a, i, 4 + 2 * h, 0);
 #pragma unroll
-          for (int ks = 0; ks < kKPad / 16; ++ks) {
+          for (int ks = 0; ks < ((a.debug & 64) ? 0 : kKPad / 16); ++ks) {
             const int kb = ks >> 2, j = ks & 3;
             const uint64_t ad = sw128_desc(at + kb * (kTileM * 128)) + 2 * j;  // +32 B per 16-element step
             const uint64_t bd = sw128_desc(w_s + kb * D * 128 + h * kUmmaN * 128) + 2 * j;
@@ -304,29 +323,38 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
     }
     __syncwarp();
   } else if (warp >= kEpiWarp0) {
-    // ---------------- epilogue: TMEM -> registers -> shared staging -> Z.
+    // ---------------- epilogue: TMEM -> registers -> swizzled shared staging -> TMA store.
     // One warp per TMEM lane quadrant (warp % 4); lane l holds row 32e + l
-    // after tcgen05.ld.  Each 128-byte slice of the 32 rows (64 bf16 / 32 fp32
-    // columns) is staged with 16-byte chunks XOR-swizzled by row (conflict-free)
-    // and written back with every store covering 4 rows x 128 contiguous bytes.
+    // after tcgen05.ld.  Each 128-byte slice of the warp's 32 rows (64 bf16 /
+    // 32 fp32 columns) is staged with 16-byte chunks XOR-swizzled by row (the
+    // TMA SWIZZLE_128B pattern, conflict-free) and written to Z by one
+    // cp.async.bulk.tensor store (box 32 rows x 128 B); two staging buffers
+    // per warp so the next slice is converted while the previous one drains.
+    // A warp whose 32 rows run past the batch (the ragged last step) or a Z
+    // without a tensor map writes the staged rows with 16-byte stores instead.
     const int e = warp & 3;                          // TMEM lane quadrant
-    const int g = (warp - kEpiWarp0) >> 2;           // column group: [g*kEpiCols, (g+1)*kEpiCols) of each 256
-    uint8_t* sbase = z_s + (warp - kEpiWarp0) * 32 * kStagePitch;
-    uint8_t* my = sbase + lane * kStagePitch;
+    uint8_t* sbuf = z_s + (warp - kEpiWarp0) * kEpiBufs * kStageBytes;
     const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
     const int cols_per_slice = 128 / a.z_elem;
-    int i = 0;
+    const uint64_t zmap_addr = reinterpret_cast<uint64_t>(&zmap);
+    int i = 0, slice = 0;
     for (int64_t t = q; t < total; t += Q) {
       int64_t step, pos;
       int r0;
       const int rows = tile_rows(t, step, r0, pos);
       if (rows <= 0) continue;
+      const bool tma_rows = a.z_tma && e * 32 + 32 <= rows;
       for (int h = 0; h < nh; ++h) {
         bar_wait(&t_full[h], i & 1);
         tc_fence_after();
         if (dbg_lane) dbg_ts(a, i, 12 + h, 0);
 #pragma unroll 1
-        for (int c0 = g * kEpiCols; c0 < ((a.debug & 4) ? g * kEpiCols : (g + 1) * kEpiCols); c0 += cols_per_slice) {
+        for (int c0 = 0; c0 < ((a.debug & 4) ? 0 : kUmmaN); c0 += cols_per_slice, ++slice) {
+          uint8_t* sb = sbuf + (slice % kEpiBufs) * kStageBytes;
+          uint8_t* my = sb + lane * 128;
+          // the bulk store issued from this buffer kEpiBufs slices ago must have read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
+          __syncwarp();
           for (int c1 = 0; c1 < cols_per_slice; c1 += 32) {  // one tcgen05.ld of 32 columns
             uint32_t v[32];
             PPL_TMEM_LD32(tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN + c0 + c1, v);
@@ -345,13 +373,25 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
                     make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
           }
-          __syncwarp();
-          {
+          if (a.debug & 2) continue;
+          if (tma_rows) {
+            fence_async_smem();  // generic-proxy staging writes -> visible to the bulk-copy engine
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                      zmap_addr),
+                  "r"(h * kUmmaN + c0), "r"(k), "r"(r0 + e * 32), "r"(static_cast<int>(step)), "r"(smem_addr(sb))
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          } else {
+            __syncwarp();
 #pragma unroll
             for (int it = 0; it < 8; ++it) {  // 4 rows x 128 contiguous bytes per instruction
               const int rr = it * 4 + (lane >> 3), ch = lane & 7;
-              const uint4 y = *reinterpret_cast<const uint4*>(sbase + rr * 128 + ((ch ^ (rr & 7)) << 4));
-              if (e * 32 + rr < rows && !(a.debug & 2)) {
+              const uint4 y = *reinterpret_cast<const uint4*>(sb + rr * 128 + ((ch ^ (rr & 7)) << 4));
+              if (e * 32 + rr < rows) {
                 uint8_t* d = a.Z + step * a.z_stride +
                              ((static_cast<int64_t>(r0 + e * 32 + rr) * H + k) * D + h * kUmmaN + c0) * a.z_elem +
                              ch * 16;
@@ -363,11 +403,12 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
         }
         if (dbg_lane) dbg_ts(a, i, 8 + 2 * h, 0);
         tc_fence_before();
-        bar_arrive(&t_empty[h]);
+        bar_arrive(&t_empty[h]);  // every tcgen05.ld of this accumulator has completed (wait::ld)
         if (dbg_lane) dbg_ts(a, i, 9 + 2 * h, 0);
       }
       ++i;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // Z writes done before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -378,16 +419,46 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_gather_linear(const LinearAr
 }
 
 size_t linear_smem_bytes(int D) {
-  return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + kEpiWarps * 32 * kStagePitch + 128;
+  return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + kEpiWarps * kEpiBufs * kStageBytes + 128;
 }
 
 bool linear_supported(int H, int F, int D, int num_sms) {
   return F >= 1 && F <= kKPad && F % 4 == 0 && (D == 256 || D == 512) && H >= 1 && H <= num_sms;
 }
 
-cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st) {
-  if (!linear_supported(a.H, a.F, a.D, a.num_sms)) return cudaErrorInvalidValue;
-  const size_t smem = linear_smem_bytes(a.D);
+namespace {
+// Z as a 4-D TMA tensor {column d, hop k, batch row j, step s} with byte strides
+// {s_z, D s_z, H D s_z, z_stride}; box = 32 rows x 128 bytes of one hop, 128-byte
+// swizzle (the epilogue's staging layout).  False when the driver entry point
+// is unavailable or the encode is rejected (the kernel then uses 16-byte stores).
+bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (encode == nullptr) return false;
+  const cuuint64_t z = static_cast<cuuint64_t>(a.z_elem);
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.H),
+                              static_cast<cuuint64_t>(a.B), static_cast<cuuint64_t>(a.nsteps)};
+  const cuuint64_t strides[3] = {a.D * z, a.H * a.D * z,
+                                 static_cast<cuuint64_t>(a.nsteps > 1 ? a.z_stride : a.B * a.H * a.D * z)};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / a.z_elem), 1, 32, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(m, a.z_elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.Z, dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t launch_gather_linear(const LinearArgs& a_in, cudaStream_t st) {
+  if (!linear_supported(a_in.H, a_in.F, a_in.D, a_in.num_sms)) return cudaErrorInvalidValue;
+  const size_t smem = linear_smem_bytes(a_in.D);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_gather_linear, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -395,8 +466,11 @@ cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  LinearArgs a = a_in;
+  alignas(64) CUtensorMap zmap{};
+  a.z_tma = (a.debug & 128) ? 0 : (encode_z_map(a, &zmap) ? 1 : 0);
   const int grid = (a.num_sms / a.H) * a.H;
-  k_gather_linear<<<grid, kLinThreads, smem, st>>>(a);
+  k_gather_linear<<<grid, kLinThreads, smem, st>>>(a, zmap);
   return cudaGetLastError();
 }
 

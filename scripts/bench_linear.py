@@ -82,8 +82,10 @@ for name, fn, bytes_per_row in (("fused_tcgen05", fused_epoch, H * F * 4 + H * D
                       "tflops": flops / ms / 1e9, "frac_tensor": flops / ms / 1e9 / PEAK_TF}), flush=True)
 L.close()
 
-if "--debug" in sys.argv:  # which stage bounds the fused kernel
-    for dbg in ("1", "2", "3"):
+if "--debug" in sys.argv:  # which stage bounds the fused kernel (bits: see LinearArgs::debug)
+    i = sys.argv.index("--debug")
+    dbgs = sys.argv[i + 1].split(",") if i + 1 < len(sys.argv) else ["1", "2", "3"]
+    for dbg in dbgs:
         os.environ["PPLOAD_DEBUG_LINEAR"] = dbg
         L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16)
         L.fill_synthetic(2504)
