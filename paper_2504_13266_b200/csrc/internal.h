@@ -97,6 +97,7 @@ struct LinearArgs {
   int64_t N, first_pos, step_stride;
   int32_t B, nsteps;
   const void* W;            // bf16 [H][F][D]
+  uint8_t* w_img;           // [H][2 K blocks][D rows][128 B] scratch: W_k^T in the UMMA layout
   int32_t H, F, D;
   uint8_t* Z;               // [nsteps][B][H][D] of z_elem bytes
   int64_t z_stride;         // bytes between step slots
@@ -105,10 +106,13 @@ struct LinearArgs {
   int32_t debug;            // experiment knob (PPLOAD_DEBUG_LINEAR), bits: 1 skip loads, 2 skip Z stores,
                             // 4 skip the drain, 8 skip A-tile stores,
                             // 64 skip MMAs, 128 no TMA stores (16-byte stores instead)
+  int32_t l2_prefetch;      // 1: bulk L2 prefetch of the next tile's rows (PPLOAD_LINEAR_PREFETCH, default 1)
   int32_t z_tma;            // set by launch_gather_linear: Z tensor map encoded, epilogue uses TMA stores
   uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null
 };
 bool linear_supported(int H, int F, int D, int num_sms);
+size_t linear_w_image_bytes(int H, int D);
+// Launches the W-image kernel, then the fused kernel, both on `st`.
 cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st);
 
 // ---- Eq. (2) propagation (propagate.cu) --------------------------------------

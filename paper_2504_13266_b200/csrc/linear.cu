@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -49,6 +50,7 @@ constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
 constexpr int kStages = 2;
 constexpr int kStageBytes = 32 * 128;  // epilogue staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
 constexpr int kEpiBufs = 2;         // staging buffers per epilogue warp
+constexpr int kWCopyChunk = 16384;  // bytes per bulk copy of the W image
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -128,6 +130,13 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // Experiment probe (LinearArgs::ts, PPLOAD_DEBUG_TS): %globaltimer at named
 // points of CTA 0's first kDbgTiles tiles, kDbgSlots per tile.
 constexpr int kDbgTiles = 24, kDbgSlots = 14;
+// after the tile slots: per CTA {entry, W copy issued, prologue done, exit}
+__device__ __forceinline__ void dbg_cta(const LinearArgs& a, int slot) {
+  if (a.ts == nullptr || threadIdx.x != 0) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  a.ts[kDbgTiles * kDbgSlots + 4 * blockIdx.x + slot] = t;
+}
 __device__ __forceinline__ void dbg_ts(const LinearArgs& a, int tile, int slot, int) {
   if (tile >= kDbgTiles) return;
   uint64_t t;
@@ -140,6 +149,7 @@ __device__ __forceinline__ void dbg_ts(const LinearArgs& a, int tile, int slot, 
 __global__ void __launch_bounds__(kLinThreads, 1)
     k_gather_linear(const LinearArgs a, const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ uint8_t smem_raw[];
+  dbg_cta(a, 0);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int D = a.D;
   uint8_t* w_s = smem;                                // [2 kb][D rows][128 B]
@@ -150,7 +160,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint64_t* a_empty = bars + kStages;                 // [kStages], MMA commit
   uint64_t* t_full = bars + 2 * kStages;              // [2], MMA commit
   uint64_t* t_empty = bars + 2 * kStages + 2;         // [2], 128 epilogue arrivals
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* w_full = bars + 2 * kStages + 4;          // W image landed (bulk copy)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, F = a.F;
@@ -167,34 +178,35 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       bar_init(&t_full[h], 1);
       bar_init(&t_empty[h], kEpiThreads);
     }
+    bar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {  // TMEM: 512 fp32 columns x 128 lanes (two 256-column accumulators)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // W_k^T into shared memory: B operand row n = output column d, K index = f
-  // (zero for f >= F).  Consecutive threads take consecutive d: coalesced reads.
-  // Each thread reads 8 consecutive d of one f with a 16-byte load and
-  // scatters them as 2-byte elements into 8 K-major rows; consecutive lanes
-  // take consecutive f so the 2-byte shared stores of a warp are contiguous.
-  const uint8_t* wk = static_cast<const uint8_t*>(a.W) + static_cast<int64_t>(k) * F * D * 2;
-  for (int idx = threadIdx.x; idx < kKPad * (D / 8); idx += kLinThreads) {
-    const int f = idx % kKPad, d0 = (idx / kKPad) * 8;
-    const uint4 w = f < F ? *reinterpret_cast<const uint4*>(wk + (static_cast<int64_t>(f) * D + d0) * 2)
-                          : make_uint4(0, 0, 0, 0);
-    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-    const int kb = f >> 6, cc = (f >> 3) & 7, fo = (f & 7) * 2;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      *reinterpret_cast<uint16_t*>(w_s + kb * D * 128 + sw128(d0 + j, cc) + fo) =
-          static_cast<uint16_t>(wv[j >> 1] >> ((j & 1) * 16));
+  // W_k^T into shared memory: one bulk copy of the hop's pre-swizzled image
+  // (k_w_image), completed on w_full; only the MMA issuer waits for it, so the
+  // producers start gathering at once.
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(2 * D * 128);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(w_full)), "r"(bytes)
+                 : "memory");
+    const uint8_t* src = a.w_img + static_cast<int64_t>(k) * bytes;
+    for (uint32_t off = 0; off < bytes; off += kWCopyChunk)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(w_s + off)),
+          "l"(src + off), "r"(kWCopyChunk), "r"(smem_addr(w_full))
+          : "memory");
   }
+  dbg_cta(a, 1);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  dbg_cta(a, 2);
 
   const int64_t tiles_per_step = (a.B + kTileM - 1) / kTileM;
   const int64_t total = tiles_per_step * a.nsteps;
@@ -278,20 +290,35 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       bar_arrive(&a_full[s]);
       if (dbg_lane) dbg_ts(a, i, 2, 0);
     };
+    // The next tile's rows are pulled into L2 with one bulk prefetch per row
+    // (no registers, no shared memory) while this tile's loads are in flight,
+    // so its own loads are L2 hits; order[] entries are fetched two tiles ahead.
+    auto prefetch_rows = [&](uint32_t idx) {
+      if (idx == kNoRow || (a.debug & 1)) return;
+      uint64_t v = idx;
+      if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
+      const uint8_t* p = a.store + static_cast<int64_t>(v) * a.rec_stride + static_cast<int64_t>(k) * F * 4;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(F * 4) : "memory");
+    };
     uint4 x[16];
     int i = 0;
     int64_t t = next_tile(q);
-    uint32_t idx = fetch_index(t);
+    int64_t t1 = t < total ? next_tile(t + Q) : total;
+    uint32_t idx = fetch_index(t), idx1 = fetch_index(t1);
     while (t < total) {
-      const int64_t tn = next_tile(t + Q);
+      const int64_t t2 = t1 < total ? next_tile(t1 + Q) : total;
       load_tile(idx, x);
-      idx = fetch_index(tn);  // in flight together with this tile's data loads
+      if (a.l2_prefetch) prefetch_rows(idx1);
+      idx = idx1;
+      idx1 = fetch_index(t2);  // in flight together with this tile's data loads
       store_tile(i++, x);
-      t = tn;
+      t = t1;
+      t1 = t2;
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (one lane)
     if (lane == 0) {
+      bar_wait(w_full, 0);
       int i = 0;
       for (int64_t t = q; t < total; t += Q) {
         int64_t step, pos;
@@ -416,7 +443,32 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+  dbg_cta(a, 3);
 }
+
+// W image: img[k][kb][n][chunk] = the 16-byte chunk of K-major row n (output
+// column d = n) holding K elements f = 64 kb + 8 c .. + 7 (zero for f >= F),
+// stored at chunk position c ^ (n & 7) (SWIZZLE_128B) -- the byte image the
+// fused kernel's B descriptors expect, so the CTA copies it verbatim.
+__global__ void k_w_image(const uint16_t* __restrict__ W, int H, int F, int D, uint8_t* __restrict__ img) {
+  const int64_t total = static_cast<int64_t>(H) * 2 * D * 8;  // 16-byte chunks
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i & 7), n = static_cast<int>((i >> 3) % D);
+    const int kb = static_cast<int>((i >> 3) / D % 2), k = static_cast<int>((i >> 3) / D / 2);
+    uint16_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int f = kb * 64 + c * 8 + j;
+      v[j] = f < F ? W[(static_cast<int64_t>(k) * F + f) * D + n] : static_cast<uint16_t>(0);
+    }
+    uint8_t* dst = img + ((static_cast<int64_t>(k) * 2 + kb) * D + n) * 128 + ((c ^ (n & 7)) << 4);
+    *reinterpret_cast<uint4*>(dst) = make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16),
+                                                v[4] | (uint32_t(v[5]) << 16), v[6] | (uint32_t(v[7]) << 16));
+  }
+}
+
+size_t linear_w_image_bytes(int H, int D) { return static_cast<size_t>(H) * 2 * D * 128; }
 
 size_t linear_smem_bytes(int D) {
   return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + kEpiWarps * kEpiBufs * kStageBytes + 128;
@@ -469,6 +521,11 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, cudaStream_t st) {
   LinearArgs a = a_in;
   alignas(64) CUtensorMap zmap{};
   a.z_tma = (a.debug & 128) ? 0 : (encode_z_map(a, &zmap) ? 1 : 0);
+  {
+    const int64_t chunks = static_cast<int64_t>(a.H) * 2 * a.D * 8;
+    const int blocks = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 4 * a.num_sms));
+    k_w_image<<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(a.W), a.H, a.F, a.D, a.w_img);
+  }
   const int grid = (a.num_sms / a.H) * a.H;
   k_gather_linear<<<grid, kLinThreads, smem, st>>>(a, zmap);
   return cudaGetLastError();

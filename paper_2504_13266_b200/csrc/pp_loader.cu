@@ -74,6 +74,8 @@ struct pp_loader {
   uint32_t* d_order = nullptr;                  // == d_orders[cur]
   uint32_t* d_pi = nullptr;
   int64_t pi_cap = 0;
+  uint8_t* d_wimg = nullptr;   // fused linear: W_k^T images in the UMMA shared-memory layout
+  size_t wimg_cap = 0;
   SortScratch sort{};
   int sort_bits_max = 0;
   int sort_bits_delta = 0;
@@ -137,6 +139,7 @@ void release(pp_loader* L) {
   cudaFree(L->d_orders[0]);
   cudaFree(L->d_orders[1]);
   cudaFree(L->d_pi);
+  cudaFree(L->d_wimg);
   cudaFree(L->sort.counts);
   cudaFree(L->sort.cursor);
   cudaFree(L->sort.blocksums);
@@ -444,6 +447,7 @@ static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint3
   } else {
     if (L->pi_cap < U) {
       cudaFree(L->d_pi);
+  cudaFree(L->d_wimg);
       L->d_pi = nullptr;
       if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
       L->pi_cap = U;
@@ -677,6 +681,15 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.B = static_cast<int32_t>(L->B);
   a.nsteps = static_cast<int32_t>(nsteps);
   a.W = W;
+  const size_t wimg = linear_w_image_bytes(L->H, D);
+  if (wimg > L->wimg_cap) {
+    cudaFree(L->d_wimg);
+    L->d_wimg = nullptr;
+    L->wimg_cap = 0;
+    PPL_CUDA(L, cudaMalloc(&L->d_wimg, wimg));
+    L->wimg_cap = wimg;
+  }
+  a.w_img = L->d_wimg;
   a.H = L->H;
   a.F = L->F;
   a.D = D;
@@ -685,16 +698,18 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.z_elem = z_elem;
   a.num_sms = L->num_sms;
   if (const char* e = getenv("PPLOAD_DEBUG_LINEAR")) a.debug = atoi(e);
+  a.l2_prefetch = 1;
+  if (const char* e = getenv("PPLOAD_LINEAR_PREFETCH")) a.l2_prefetch = atoi(e);
   static uint64_t* dbg_ts = nullptr;  // experiment probe: timestamps of CTA 0 (PPLOAD_DEBUG_TS=1)
   const bool want_ts = getenv("PPLOAD_DEBUG_TS") != nullptr;
-  if (want_ts && !dbg_ts) PPL_CUDA(L, cudaMalloc(&dbg_ts, 24 * 14 * 8));
+  if (want_ts && !dbg_ts) PPL_CUDA(L, cudaMalloc(&dbg_ts, (24 * 14 + 4 * 1024) * 8));
   if (want_ts) {
-    PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, 24 * 14 * 8, L->stream));
+    PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, (24 * 14 + 4 * 1024) * 8, L->stream));
     a.ts = dbg_ts;
   }
   PPL_CUDA(L, launch_gather_linear(a, L->stream));
   if (want_ts) {
-    uint64_t h[24 * 14];
+    static uint64_t h[24 * 14 + 4 * 1024];
     PPL_CUDA(L, cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, L->stream));
     PPL_CUDA(L, cudaStreamSynchronize(L->stream));
     const uint64_t t0 = h[0];
@@ -704,6 +719,19 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
         fprintf(stderr, " %7.2f", h[t * 14 + s] ? (double)(int64_t)(h[t * 14 + s] - t0) / 1e3 : -1.0);
       fprintf(stderr, "\n");
     }
+    // per-CTA entry / prologue done / exit, relative to the earliest entry
+    const int nb = (L->num_sms / L->H) * L->H;
+    uint64_t e0 = UINT64_MAX;
+    for (int b = 0; b < nb; ++b) e0 = std::min(e0, h[24 * 14 + 4 * b]);
+    double mx[4] = {0, 0, 0, 0}, sm[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < 4; ++j) {
+        const double v = (double)(int64_t)(h[24 * 14 + 4 * b + j] - e0) / 1e3;
+        mx[j] = std::max(mx[j], v);
+        sm[j] += v / nb;
+      }
+    fprintf(stderr, "cta us (mean/max): entry %.2f/%.2f w_staged %.2f/%.2f prologue_done %.2f/%.2f exit %.2f/%.2f\n",
+            sm[0], mx[0], sm[1], mx[1], sm[2], mx[2], sm[3], mx[3]);
   }
   L->last_was_gather = false;
   if (handoff) {

@@ -16,7 +16,7 @@ ge.build()
 import paper_2504_13266_b200 as pp  # noqa: E402
 
 N, H, F, B, D = 2_449_029, 4, 100, 8192, 512
-K = 8  # steps per launch
+K = int(os.environ.get("LIN_K", "8"))  # steps per launch
 PEAK_HBM = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 PEAK_TF = json.load(open("MEASURED_PEAKS.json"))["bf16_tflops"] if os.path.exists("MEASURED_PEAKS.json") else 1590.0
 L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16)
@@ -26,7 +26,7 @@ L.set_stream(st)
 steps = L.query()["steps_per_epoch"]
 rng = np.random.default_rng(0)
 W = torch.from_numpy((rng.standard_normal((H, F, D)) / 10).astype(np.float32)).cuda().to(torch.bfloat16)
-nslots = 16
+nslots = max(16, 2 * K)
 Z = torch.empty((nslots, B, H, D), dtype=torch.bfloat16, device="cuda")
 X = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
 Zh = torch.empty((nslots, H, B, D), dtype=torch.bfloat16, device="cuda")  # unfused output, hop-major
