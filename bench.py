@@ -290,13 +290,16 @@ def run_ours(args):
                     "algorithmic_bytes_per_node": rec_in + rec_out + 4,
                     "frac_of_8TBs_nominal": m["achieved"] / 8000.0}
     else:
-        # pull design: (W-1)/W of each rank's rows arrive over NVLink as fp32 records
-        nvl = m["bytes_per_launch"] / (rec_in + rec_out + 4) * rec_in * (W - 1) / W
+        # pull design: (W-1)/W of each rank's rows arrive over NVLink, read from the owner's
+        # exchange copy (already cast: rec_out bytes) or, without one, as fp32 records (rec_in)
+        rec_nvl = rec_out if L.query()["exchange_cast"] else rec_in
+        nvl = m["bytes_per_launch"] / (rec_in + rec_out + 4) * rec_nvl * (W - 1) / W
         achieved = nvl / (m["per_launch_ms"] / 1e3) / 1e9
         roofline = {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s", "frac": achieved / 770.0,
                     "traffic": None, "kernel": "k_gather_tma<bf16, sharded>",
                     "peak_kind": "guide-measured peer copy per direction (B200_PROFILING.md)",
-                    "algorithmic_nvlink_bytes_per_node": rec_in * (W - 1) / W, "hbm_GBs": m["achieved"]}
+                    "algorithmic_nvlink_bytes_per_node": rec_nvl * (W - 1) / W, "hbm_GBs": m["achieved"],
+                    "exchange_cast": bool(L.query()["exchange_cast"])}
     roofline.update({"per_launch_us": m["per_launch_ms"] * 1e3, "algorithmic_bytes_per_launch": m["bytes_per_launch"],
                      "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
                              "(includes launch gaps and the overlapped next-epoch permutation)"})

@@ -48,7 +48,10 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 1
+#define PP_ABI_VERSION 2
+
+/* Bytes of one rank's exported store handle (pp_export_store). */
+#define PP_IPC_HANDLE_BYTES 128
 
 typedef struct pp_loader pp_loader; /* opaque handle */
 
@@ -129,6 +132,9 @@ typedef struct {
   int32_t gather_path;      /* 0 = vector (16-B) path, 1 = scalar fallback */
   int32_t local_epoch;      /* 1 if the current epoch came from pp_epoch_permute_local */
   int64_t epoch_positions;  /* positions of the current epoch (N, or local_rows when local) */
+  int32_t exchange_cast;    /* 1: this rank keeps a cast exchange copy of its HBM rows that the
+                               peers read instead of the fp32 records (W > 1, see below) */
+  int32_t reserved0;
 } pp_loader_info;
 
 /* Create a loader.  Copies the hop data into a library-owned, node-major store
@@ -254,11 +260,23 @@ int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_byt
 
 /* ---- multi-GPU plumbing (W > 1) ------------------------------------------ */
 
-/* PP_PEERS_IPC: write this rank's store handle (64 opaque bytes) to
- * handle_out; the caller all-gathers the W handles (e.g. torch.distributed)
- * and passes them, rank-ordered, to pp_import_peer_stores on every rank. */
+/* Exchange copy (W > 1, fp32 store -> 16-bit batches).  Each rank keeps, next
+ * to its fp32 shard, a copy of its HBM rows already cast to the batch dtype
+ * (the same RNE cast as the gather, written at create and by
+ * pp_fill_synthetic).  Peers read a remote row from that copy, so NVLink
+ * carries H*F*s_out bytes per remote row -- the cast-before-transfer traffic
+ * of an owner-side push -- while local rows are still read
+ * in fp32 and cast inside the gather.  It costs s_out/s_in of the shard in
+ * HBM; a rank that cannot fit it (or runs with PPLOAD_EXCHANGE_CAST=0) simply
+ * exports none and its peers pull its fp32 records.  Batches are bit-identical
+ * either way (pp_loader_info.exchange_cast reports the choice).
+ *
+ * PP_PEERS_IPC: write this rank's handle (PP_IPC_HANDLE_BYTES opaque bytes:
+ * the store and, if present, the exchange copy) to handle_out; the caller
+ * all-gathers the W handles (e.g. torch.distributed) and passes them,
+ * rank-ordered, to pp_import_peer_stores on every rank. */
 pp_status pp_export_store(pp_loader* L, void* handle_out);
-pp_status pp_import_peer_stores(pp_loader* L, const void* handles /* W*64 bytes */);
+pp_status pp_import_peer_stores(pp_loader* L, const void* handles /* W*PP_IPC_HANDLE_BYTES bytes */);
 
 /* PP_PEERS_LOOPBACK: link W handles of one process (same device), rank-ordered. */
 pp_status pp_link_loopback(pp_loader* const* loaders, int32_t world_size);

@@ -215,8 +215,11 @@ def pp_link_loopback(handles) -> None:
     _check(lib().pp_link_loopback(arr, len(handles)), "pp_link_loopback")
 
 
+IPC_HANDLE_BYTES = 128  # PP_IPC_HANDLE_BYTES
+
+
 def pp_export_store(h) -> bytes:
-    buf = ctypes.create_string_buffer(64)
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
     _check(lib().pp_export_store(h, buf), "pp_export_store")
     return buf.raw
 

@@ -75,6 +75,8 @@ class pp_loader_info(ctypes.Structure):
         ("gather_path", ctypes.c_int32),
         ("local_epoch", ctypes.c_int32),
         ("epoch_positions", ctypes.c_int64),
+        ("exchange_cast", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
 

@@ -92,7 +92,10 @@ __device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, 
     }
     const ShardView sh = a.shards[owner];
     const int64_t l = static_cast<int64_t>(lr);
-    s_src[threadIdx.x] = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
+    if (SHARDED && sh.xhbm != nullptr && l < sh.n_hbm)  // peer row, already cast: bit 0 marks it
+      s_src[threadIdx.x] = sh.xhbm + l * a.xrec_stride + 1;
+    else
+      s_src[threadIdx.x] = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
     const int64_t oj = step * a.B + j0 + threadIdx.x;
     if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
     if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
@@ -126,15 +129,23 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
     const uint32_t nvec = static_cast<uint32_t>(rows) * vpr;
     for (uint32_t e0 = threadIdx.x; e0 < nvec; e0 += kGatherThreads * kUnroll) {
       uint4 x0[kUnroll], x1[kUnroll];
+      bool pre[kUnroll];  // slot of a peer's exchange copy: 16 bytes already in the batch dtype
 #pragma unroll
       for (int q = 0; q < kUnroll; ++q) {
         const uint32_t e = e0 + q * kGatherThreads;
+        pre[q] = false;
         if (e < nvec) {
           const uint32_t r = fast_div(e, vpr_M);
           const uint32_t c = e - r * vpr;
-          const uint8_t* src = s_src[buf][r] + static_cast<int64_t>(c) * kInBytes;
-          x0[q] = ld_stream(src, a.l2_prefetch);
-          if (MODE != kModeCopy) x1[q] = ld_stream(src + 16, a.l2_prefetch);
+          const uint8_t* row = s_src[buf][r];
+          if (SHARDED && MODE != kModeCopy && (reinterpret_cast<uintptr_t>(row) & 1u)) {
+            pre[q] = true;
+            x0[q] = ld_stream(row - 1 + static_cast<int64_t>(c) * 16, a.l2_prefetch);
+          } else {
+            const uint8_t* src = row + static_cast<int64_t>(c) * kInBytes;
+            x0[q] = ld_stream(src, a.l2_prefetch);
+            if (MODE != kModeCopy) x1[q] = ld_stream(src + 16, a.l2_prefetch);
+          }
         }
       }
 #pragma unroll
@@ -145,7 +156,9 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
           const uint32_t c = e - r * vpr;
           uint8_t* dst = out_tile + static_cast<int64_t>(r) * row_out_bytes + static_cast<int64_t>(c) * 16;
           uint4 y;
-          if (MODE == kModeBF16) {
+          if (SHARDED && pre[q]) {
+            y = x0[q];
+          } else if (MODE == kModeBF16) {
             y = make_uint4(pack_bf16(x0[q].x, x0[q].y), pack_bf16(x0[q].z, x0[q].w), pack_bf16(x1[q].x, x1[q].y),
                            pack_bf16(x1[q].z, x1[q].w));
           } else if (MODE == kModeF16) {
@@ -254,6 +267,7 @@ __global__ void __launch_bounds__(kGatherThreads, 2)
                  int32_t tr) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kTmaStages];
+  __shared__ uint8_t s_pre[kTmaStages][32];  // row holds a peer's exchange copy (already cast)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kInBytes = (MODE == kModeCopy) ? 16 : 32;
   const int64_t tiles_per_step = (a.B + tr - 1) / tr;
@@ -284,11 +298,14 @@ __global__ void __launch_bounds__(kGatherThreads, 2)
     if (rows <= 0) return;
     const int s = static_cast<int>(k % kTmaStages);
     uint8_t* stage = smem + s * stage_bytes;
-    if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * rec_in);
-    __syncwarp();
-    for (int j = lane; j < rows; j += 32) {
+    // rows <= 16 <= 32: lane j resolves row j, the warp sums the bytes for expect_tx
+    const int j = lane;
+    const uint8_t* src = nullptr;
+    uint32_t bytes = 0;
+    uint64_t v = 0;
+    if (j < rows) {
       const int64_t p = step_pos + j0 + j;
-      uint64_t v = a.order[p];
+      v = a.order[p];
       if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
       int owner = 0;
       uint64_t lr = v;
@@ -298,8 +315,17 @@ __global__ void __launch_bounds__(kGatherThreads, 2)
       }
       const ShardView sh = a.shards[owner];
       const int64_t l = static_cast<int64_t>(lr);
-      const uint8_t* src = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
-      bulk_g2s(stage + static_cast<int64_t>(j) * rec_in, src, static_cast<uint32_t>(rec_in), &full[s]);
+      const bool pre = SHARDED && MODE != kModeCopy && sh.xhbm != nullptr && l < sh.n_hbm;
+      src = pre ? sh.xhbm + l * a.xrec_stride
+                : (l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride);
+      bytes = static_cast<uint32_t>(pre ? rec_in / 2 : rec_in);
+      s_pre[s][j] = pre ? 1 : 0;
+    }
+    const uint32_t total_bytes = __reduce_add_sync(0xffffffffu, bytes);
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], total_bytes);
+    __syncwarp();
+    if (j < rows) {
+      bulk_g2s(stage + static_cast<int64_t>(j) * rec_in, src, bytes, &full[s]);
       const int64_t oj = step * a.B + j0 + j;
       if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
       if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
@@ -325,7 +351,9 @@ __global__ void __launch_bounds__(kGatherThreads, 2)
         const uint32_t c = e - r * vpr;
         const uint4* src = reinterpret_cast<const uint4*>(stage + static_cast<int64_t>(r) * rec_in + c * kInBytes);
         uint4 y;
-        if (MODE == kModeBF16) {
+        if (SHARDED && MODE != kModeCopy && s_pre[s][r]) {
+          y = reinterpret_cast<const uint4*>(stage + static_cast<int64_t>(r) * rec_in)[c];
+        } else if (MODE == kModeBF16) {
           const uint4 x0 = src[0], x1 = src[1];
           y = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
         } else if (MODE == kModeF16) {
@@ -349,6 +377,39 @@ static int tma_rows_per_stage(int64_t rec_in) {
   if (tr < 1) tr = 1;
   if (tr > 16) tr = 16;
   return static_cast<int>(tr);
+}
+
+// Exchange copy: one thread per 16-byte output vector (8 elements).
+template <int MODE>
+__global__ void k_cast_records(const uint8_t* __restrict__ src, int64_t rows, int64_t rec_stride, uint32_t vpr,
+                               uint8_t* __restrict__ dst, int64_t xrec_stride) {
+  const int64_t total = rows * vpr;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vpr, c = i - r * vpr;
+    const uint8_t* p = src + r * rec_stride + c * 32;
+    const uint4 x0 = ld_stream(p), x1 = ld_stream(p + 16);
+    uint4 y;
+    if (MODE == kModeBF16)
+      y = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
+    else
+      y = make_uint4(pack_f16(x0.x, x0.y), pack_f16(x0.z, x0.w), pack_f16(x1.x, x1.y), pack_f16(x1.z, x1.w));
+    st_vec(dst + r * xrec_stride + c * 16, y);
+  }
+}
+
+cudaError_t launch_cast_records(const uint8_t* src, int64_t rows, int64_t rec_stride, int32_t HF, int32_t out_dtype,
+                                uint8_t* dst, int64_t xrec_stride, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  if (HF % 8 != 0 || (out_dtype != kBF16 && out_dtype != kF16)) return cudaErrorInvalidValue;
+  const uint32_t vpr = static_cast<uint32_t>(HF / 8);
+  const int64_t total = rows * vpr;
+  const int blocks = static_cast<int>(total / 256 + 1 < 148 * 16 ? total / 256 + 1 : 148 * 16);
+  if (out_dtype == kBF16)
+    k_cast_records<kModeBF16><<<blocks, 256, 0, st>>>(src, rows, rec_stride, vpr, dst, xrec_stride);
+  else
+    k_cast_records<kModeF16><<<blocks, 256, 0, st>>>(src, rows, rec_stride, vpr, dst, xrec_stride);
+  return cudaGetLastError();
 }
 
 bool gather_vector_ok(int32_t HF, int32_t in_dtype, int32_t out_dtype, int64_t rec_stride) {

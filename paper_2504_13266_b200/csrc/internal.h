@@ -12,10 +12,14 @@ constexpr int kMaxWorld = 8;
 // Where the rows owned by one rank live: local row lr < n_hbm at
 // hbm + lr * rec_stride, otherwise at spill + (lr - n_hbm) * rec_stride
 // (spill = device alias of pinned, mapped host memory: UVA zero-copy).
+// xhbm: the owner's exchange copy (rows < n_hbm already cast to the batch
+// dtype, pitch GatherArgs::xrec_stride) that a peer reads instead of the fp32
+// record; null for the reader's own shard or when the owner has none.
 struct ShardView {
   const uint8_t* hbm;
   const uint8_t* spill;
   int64_t n_hbm;
+  const uint8_t* xhbm = nullptr;
 };
 
 // ---- permutation (permute.cu) ------------------------------------------------
@@ -72,6 +76,7 @@ struct GatherArgs {
   int32_t W;
   ShardView shards[kMaxWorld];
   int64_t rec_stride;       // store pitch (bytes)
+  int64_t xrec_stride;      // exchange-copy pitch (bytes), see ShardView::xhbm
   int32_t HF;               // elements per record
   int32_t in_dtype, out_dtype;  // pp_dtype codes
   int32_t tile_rows;        // batch rows per CTA tile (1..32)
@@ -120,6 +125,12 @@ cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int6
                                    cudaStream_t st);
 cudaError_t launch_spmm(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col, const double* val,
                         const float* x, float* y, cudaStream_t st);
+
+// ---- exchange copy (gather.cu) ----------------------------------------------
+// dst[r] = cast(src[r]) for rows [0, rows): fp32 records (pitch rec_stride) ->
+// 16-bit records (pitch xrec_stride), the gather's RNE cast.  HF % 8 == 0.
+cudaError_t launch_cast_records(const uint8_t* src, int64_t rows, int64_t rec_stride, int32_t HF, int32_t out_dtype,
+                                uint8_t* dst, int64_t xrec_stride, cudaStream_t st);
 
 // ---- synthetic fill (gather.cu) ---------------------------------------------
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,

@@ -65,6 +65,8 @@ struct pp_loader {
   uint8_t* d_store = nullptr;
   uint8_t* h_spill = nullptr;
   uint8_t* d_spill = nullptr;  // device alias of h_spill
+  uint8_t* d_xstore = nullptr;  // exchange copy: HBM rows cast to out_dtype, read by the peers (W > 1)
+  int64_t xrec_stride = 0;      // its pitch (same on every rank; 0 when the dtype pair has no cast)
   int64_t* d_node_set = nullptr;
   int32_t* d_labels = nullptr;
   bool has_labels = false;
@@ -132,6 +134,7 @@ void release(pp_loader* L) {
   if (L->stream) cudaStreamSynchronize(L->stream);
   for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(L->d_store);
+  cudaFree(L->d_xstore);
   if (L->h_spill) cudaFreeHost(L->h_spill);
   cudaFree(L->d_node_set);
   cudaFree(L->d_labels);
@@ -219,6 +222,15 @@ pp_status validate(const pp_loader_desc* d) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || d->device < 0 || d->device >= ndev)
     return fail(PP_ERR_INVALID, "device %d not available", d->device);
   return PP_OK;
+}
+
+// Rewrite the exchange copy from the HBM rows of the store (after any store write).
+cudaError_t refresh_exchange_copy(pp_loader* L) {
+  if (!L->d_xstore) return cudaSuccess;
+  cudaError_t e = launch_cast_records(L->d_store, L->n_hbm, L->rec_stride, L->HF, L->out_dtype, L->d_xstore,
+                                      L->xrec_stride, L->stream ? L->stream : 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream ? L->stream : 0);
+  return e;
 }
 
 pp_status ensure_sort_scratch(pp_loader* L, uint32_t U, int bits) {
@@ -332,6 +344,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     release(L);
     return s;
   };
+  cudaError_t e_x = cudaSuccess;
 
   // ---- placement: HBM budget, remainder spills to pinned mapped host memory
   const int64_t scratch = L->N * 4 * 3 + (int64_t(1) << 26) + (L->has_labels ? L->N_total * 4 : 0);
@@ -405,6 +418,19 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
   L->linked = (L->W == 1);
+  // ---- exchange copy for the peers (see pp_loader.h): only if it fits after everything else
+  if (L->W > 1 && L->in_dtype == PP_F32 && L->out_dtype != PP_F32 && L->vector_path) {
+    L->xrec_stride = (L->rec_out + 15) / 16 * 16;
+    const char* env = getenv("PPLOAD_EXCHANGE_CAST");
+    size_t fr = 0, tot = 0;
+    const size_t xbytes = static_cast<size_t>(L->n_hbm) * L->xrec_stride;
+    if (L->n_hbm > 0 && !(env && !strcmp(env, "0")) && cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
+        fr > xbytes + (size_t(1) << 30)) {
+      if (cudaMalloc(&L->d_xstore, xbytes) != cudaSuccess) return bail(fail(PP_ERR_OOM, "exchange copy allocation"));
+      if (desc->hops.data && (e_x = refresh_exchange_copy(L)) != cudaSuccess)
+        return bail(fail(PP_ERR_CUDA, "exchange copy: %s", cudaGetErrorString(e_x)));
+    }
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PP_ERR_CUDA, "create sync"));
   *out = L;
   return PP_OK;
@@ -601,6 +627,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   a.W = L->W;
   for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = L->shards[i];
   a.rec_stride = L->rec_stride;
+  a.xrec_stride = L->xrec_stride;
   a.HF = L->HF;
   a.in_dtype = L->in_dtype;
   a.out_dtype = L->out_dtype;
@@ -769,6 +796,8 @@ pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
   info->gather_path = L->vector_path ? 0 : 1;
   info->local_epoch = L->local ? 1 : 0;
   info->epoch_positions = L->local ? L->local_rows : L->N;
+  info->exchange_cast = L->d_xstore != nullptr ? 1 : 0;
+  info->reserved0 = 0;
   return PP_OK;
 }
 
@@ -782,6 +811,7 @@ pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed) {
   PPL_CUDA(L, launch_fill_synthetic(L->d_spill, L->n_hbm, L->n_spill, L->rec_stride, L->H, L->F, L->in_dtype,
                                     data_seed, L->W, L->rank, L->stream));
   PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+  PPL_CUDA(L, refresh_exchange_copy(L));
   return PP_OK;
 }
 
@@ -819,10 +849,15 @@ pp_status pp_export_store(pp_loader* L, void* handle_out) {
   if (!L || !handle_out) return fail(PP_ERR_INVALID, "NULL argument");
   if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_export_store needs PP_PEERS_IPC");
   DevGuard g(L->dev);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64 && PP_IPC_HANDLE_BYTES == 128, "IPC handle layout");
   cudaIpcMemHandle_t h;
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_store));
-  memcpy(handle_out, &h, 64);
+  memcpy(handle_out, &h, 64);  // [0, 64): the store; [64, 128): the exchange copy, or zeros
+  memset(static_cast<uint8_t*>(handle_out) + 64, 0, 64);
+  if (L->d_xstore) {
+    PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_xstore));
+    memcpy(static_cast<uint8_t*>(handle_out) + 64, &h, 64);
+  }
   return PP_OK;
 }
 
@@ -833,13 +868,22 @@ pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
   DevGuard g(L->dev);
   for (int o = 0; o < L->W; ++o) {
     if (o == L->rank) continue;
+    const uint8_t* rec = static_cast<const uint8_t*>(handles) + PP_IPC_HANDLE_BYTES * o;
     cudaIpcMemHandle_t h;
-    memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * o, 64);
+    memcpy(&h, rec, 64);
     void* p = nullptr;
     PPL_CUDA(L, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     L->ipc_opened.push_back(p);
+    void* x = nullptr;
+    bool has_x = false;
+    for (int i = 64; i < 128; ++i) has_x |= rec[i] != 0;
+    if (has_x && L->xrec_stride > 0) {  // the owner keeps an exchange copy: read remote rows from it
+      memcpy(&h, rec + 64, 64);
+      PPL_CUDA(L, cudaIpcOpenMemHandle(&x, h, cudaIpcMemLazyEnablePeerAccess));
+      L->ipc_opened.push_back(x);
+    }
     const int64_t rows_o = (L->N_total - o + L->W - 1) / L->W;  // whole shard in HBM (checked at create)
-    L->shards[o] = ShardView{static_cast<const uint8_t*>(p), nullptr, rows_o};
+    L->shards[o] = ShardView{static_cast<const uint8_t*>(p), nullptr, rows_o, static_cast<const uint8_t*>(x)};
   }
   L->linked = true;
   return PP_OK;
@@ -853,11 +897,13 @@ pp_status pp_link_loopback(pp_loader* const* Ls, int32_t W) {
     if (L->desc.peers != PP_PEERS_LOOPBACK || L->W != W || L->rank != r)
       return fail(PP_ERR_INVALID, "loader %d: not a loopback rank %d of %d", r, r, W);
     if (L->dev != Ls[0]->dev || L->H != Ls[0]->H || L->F != Ls[0]->F || L->in_dtype != Ls[0]->in_dtype ||
-        L->N_total != Ls[0]->N_total || L->rec_stride != Ls[0]->rec_stride)
+        L->N_total != Ls[0]->N_total || L->rec_stride != Ls[0]->rec_stride ||
+        L->out_dtype != Ls[0]->out_dtype || L->xrec_stride != Ls[0]->xrec_stride)
       return fail(PP_ERR_INVALID, "loader %d: store shape differs from rank 0", r);
   }
   for (int r = 0; r < W; ++r) {
-    for (int o = 0; o < W; ++o) Ls[r]->shards[o] = ShardView{Ls[o]->d_store, Ls[o]->d_spill, Ls[o]->n_hbm};
+    for (int o = 0; o < W; ++o)
+      Ls[r]->shards[o] = ShardView{Ls[o]->d_store, Ls[o]->d_spill, Ls[o]->n_hbm, o == r ? nullptr : Ls[o]->d_xstore};
     Ls[r]->linked = true;
   }
   return PP_OK;

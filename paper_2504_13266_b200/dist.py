@@ -10,15 +10,15 @@ import hashlib
 
 import torch.distributed as dist
 
-from . import pp_export_store, pp_import_peer_stores
+from . import IPC_HANDLE_BYTES, pp_export_store, pp_import_peer_stores
 
-HANDLE_BYTES = 64
+HANDLE_BYTES = IPC_HANDLE_BYTES
 
 
 def exchange_handles(local: bytes, group=None) -> bytes:
-    """All-gather every rank's 64-byte store handle; returns them rank-ordered, concatenated."""
+    """All-gather every rank's store handle (HANDLE_BYTES bytes); returns them rank-ordered, concatenated."""
     if len(local) != HANDLE_BYTES:
-        raise ValueError("store handles are 64 bytes")
+        raise ValueError(f"store handles are {HANDLE_BYTES} bytes")
     W = dist.get_world_size(group)
     out = [None] * W
     dist.all_gather_object(out, local, group=group)

@@ -43,8 +43,17 @@ def test_built_for_sm100a(pp):
     assert "sm_100a" in out.stdout
 
 
+def _header_define(name):
+    import re
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "pp_loader.h")).read()
+    return int(re.search(rf"#define {name} (\d+)", hdr).group(1))
+
+
 def test_abi_version_and_footprint(pp):
-    assert pp.pp_abi_version() == 1
+    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 2
+    assert pp.IPC_HANDLE_BYTES == _header_define("PP_IPC_HANDLE_BYTES")
     # input expansion K(R+1)x: 400 GB at R = 3, K = 1 -> 1.6 TB
     n = 100_000_000
     assert pp.pp_footprint_bytes(n, 1000, 4, 1, 0) == 400 * 10**9

@@ -21,8 +21,9 @@ def _worker(rank, world, port, q):
     try:
         from paper_2504_13266_b200 import dist as ppd
 
-        hs = ppd.exchange_handles(bytes([rank]) * 64)
-        ok_handles = hs == b"".join(bytes([r]) * 64 for r in range(world))
+        n = ppd.HANDLE_BYTES
+        hs = ppd.exchange_handles(bytes([rank]) * n)
+        ok_handles = hs == b"".join(bytes([r]) * n for r in range(world))
         ppd.check_epoch_args(250413266, 8192)
         try:
             ppd.check_epoch_args(250413266 + rank, 8192)

@@ -20,9 +20,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, chunk, q):
+def _worker(rank, world, port, chunk, xcast, q):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PPLOAD_EXCHANGE_CAST=str(xcast[rank]))
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -38,6 +38,7 @@ def _worker(rank, world, port, chunk, q):
         X, hs, rs = hop_tensor(40, H, N, F)
         L = pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
                       batch_size=B, out_dtype=pp.PP_BF16, world_size=world, rank=rank, peers=pp.PP_PEERS_IPC)
+        has_x = L.query()["exchange_cast"]
         ppd.link_ipc(L)
         ppd.check_epoch_args(17, chunk)
         L.epoch_permute(17, chunk)
@@ -54,15 +55,17 @@ def _worker(rank, world, port, chunk, q):
             t += 1
         dist.barrier()  # peers keep their stores alive until everyone is done
         L.close()
-        q.put((rank, bad, t == oracle.num_steps(N, B, world)))
+        q.put((rank, bad, t == oracle.num_steps(N, B, world), has_x))
     except Exception as e:  # pragma: no cover - reported through the queue
-        q.put((rank, repr(e), False))
+        q.put((rank, repr(e), False, None))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunk", [1, 64])
-def test_ipc_two_processes_one_gpu(chunk):
+# xcast: per-rank PPLOAD_EXCHANGE_CAST -- peers read the owner's cast exchange copy (1) or its fp32
+# records (0); mixed ranks exercise both in one epoch.  Batches are bit-identical either way.
+@pytest.mark.parametrize("chunk,xcast", [(1, (1, 1)), (64, (1, 1)), (1, (0, 0)), (64, (1, 0))])
+def test_ipc_two_processes_one_gpu(chunk, xcast):
     import torch.multiprocessing as mp
 
     import __graft_entry__ as ge
@@ -71,11 +74,12 @@ def test_ipc_two_processes_one_gpu(chunk):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, chunk, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, chunk, xcast, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
     for p in procs:
         p.join(timeout=60)
-    for rank, bad, steps_ok in res:
+    for rank, bad, steps_ok, has_x in res:
         assert bad == 0 and steps_ok, (rank, bad)
+        assert has_x == xcast[rank]
