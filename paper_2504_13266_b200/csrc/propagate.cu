@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -77,6 +79,69 @@ __global__ void __launch_bounds__(256) k_spmm_rows(int64_t n, int32_t F, const i
   }
 }
 
+// Vector variant (F % 4 == 0): lane l owns features 4l..4l+3 (+ 128 + 4l.. for
+// FV = 2), so a neighbour row is one 16-byte load per lane instead of up to four
+// 4-byte loads, and kAhead neighbour rows are loaded before any is accumulated
+// (their addresses do not depend on the sums).  The additions still run in
+// ascending column order per output element: bit-identical to k_spmm_rows.
+template <int FV>
+__global__ void __launch_bounds__(256) k_spmm_rows_v4(int64_t n, int32_t F, const int64_t* __restrict__ row_ptr,
+                                                      const int64_t* __restrict__ col, const double* __restrict__ val,
+                                                      const float* __restrict__ x, float* __restrict__ y) {
+  constexpr int kAhead = 4;
+  const int lane = threadIdx.x & 31;
+  const int nv = F >> 2;  // float4 per row
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < n;
+       i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+    double acc[FV][4];
+#pragma unroll
+    for (int q = 0; q < FV; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[q][c] = 0.0;
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const int m = static_cast<int>(min(static_cast<int64_t>(32), e - p0));
+      const int64_t jl = lane < m ? col[p0 + lane] : 0;
+      const double wl = lane < m ? val[p0 + lane] : 0.0;
+      for (int s0 = 0; s0 < m; s0 += kAhead) {
+        float4 xv[kAhead][FV];
+        double w[kAhead];
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+          const int s = s0 + u < m ? s0 + u : m - 1;
+          const int64_t j = __shfl_sync(0xffffffffu, jl, s);
+          w[u] = __shfl_sync(0xffffffffu, wl, s);
+          const float4* xr = reinterpret_cast<const float4*>(x + j * F);
+#pragma unroll
+          for (int q = 0; q < FV; ++q) {
+            const int v = lane + 32 * q;
+            xv[u][q] = (s0 + u < m && v < nv) ? __ldg(xr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+          if (s0 + u >= m) break;
+#pragma unroll
+          for (int q = 0; q < FV; ++q) {
+            acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(w[u], static_cast<double>(xv[u][q].x)));
+            acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(w[u], static_cast<double>(xv[u][q].y)));
+            acc[q][2] = __dadd_rn(acc[q][2], __dmul_rn(w[u], static_cast<double>(xv[u][q].z)));
+            acc[q][3] = __dadd_rn(acc[q][3], __dmul_rn(w[u], static_cast<double>(xv[u][q].w)));
+          }
+        }
+      }
+    }
+    float4* yr = reinterpret_cast<float4*>(y + i * F);
+#pragma unroll
+    for (int q = 0; q < FV; ++q) {
+      const int v = lane + 32 * q;
+      if (v < nv)
+        yr[v] = make_float4(__double2float_rn(acc[q][0]), __double2float_rn(acc[q][1]), __double2float_rn(acc[q][2]),
+                            __double2float_rn(acc[q][3]));
+    }
+  }
+}
+
 cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int64_t* col, double* val,
                                    cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -89,7 +154,11 @@ cudaError_t launch_spmm(int64_t n, int32_t F, const int64_t* row_ptr, const int6
   if (n <= 0 || F <= 0) return cudaSuccess;
   const int64_t warps = n;
   const int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, 148ll * 64);
-  if (F <= 32) k_spmm_rows<1><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  const bool vec = F % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+                   !(getenv("PPLOAD_SPMM") && !strcmp(getenv("PPLOAD_SPMM"), "scalar"));
+  if (vec && F <= 128) k_spmm_rows_v4<1><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  else if (vec && F <= 256) k_spmm_rows_v4<2><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  else if (F <= 32) k_spmm_rows<1><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 64) k_spmm_rows<2><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 128) k_spmm_rows<4><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 256) k_spmm_rows<8><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);

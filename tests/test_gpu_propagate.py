@@ -91,3 +91,19 @@ def test_invalid_arguments(pp):
     with pytest.raises(pp.PPError) as ei:
         pp.pp_propagate(rp, ci, X, 1, hops)  # row_ptr[n] = 0 < n: no diagonal
     assert ei.value.status == pp.PP_ERR_INVALID
+
+
+@pytest.mark.parametrize("F", [4, 100, 132, 256])
+def test_scalar_and_vector_kernels_agree(pp, monkeypatch, F):
+    # F % 4 == 0 takes the 16-byte-per-lane kernel; PPLOAD_SPMM=scalar forces the per-element one.
+    # Both sum in ascending column order, so both equal the oracle bit for bit.
+    n, m = 900, 7000
+    rng = np.random.default_rng(F)
+    rp, ci = oracle.build_csr(n, rng.integers(0, n, m), rng.integers(0, n, m))
+    X = rng.standard_normal((n, F)).astype(np.float32)
+    want = oracle.propagate(n, rp, ci, oracle.operator_values(n, rp, ci), X, 2)
+    vec = gpu_propagate(pp, rp, ci, X, 2)
+    monkeypatch.setenv("PPLOAD_SPMM", "scalar")
+    sca = gpu_propagate(pp, rp, ci, X, 2)
+    assert np.array_equal(vec.view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(sca.view(np.uint32), want.view(np.uint32))
