@@ -84,11 +84,10 @@ __global__ void __launch_bounds__(256) k_spmm_rows(int64_t n, int32_t F, const i
 // 4-byte loads, and kAhead neighbour rows are loaded before any is accumulated
 // (their addresses do not depend on the sums).  The additions still run in
 // ascending column order per output element: bit-identical to k_spmm_rows.
-template <int FV>
-__global__ void __launch_bounds__(256) k_spmm_rows_v4(int64_t n, int32_t F, const int64_t* __restrict__ row_ptr,
+template <int FV, int kAhead>
+__global__ void __launch_bounds__(256, (FV == 1 && kAhead == 4) ? 4 : 1) k_spmm_rows_v4(int64_t n, int32_t F, const int64_t* __restrict__ row_ptr,
                                                       const int64_t* __restrict__ col, const double* __restrict__ val,
                                                       const float* __restrict__ x, float* __restrict__ y) {
-  constexpr int kAhead = 4;
   const int lane = threadIdx.x & 31;
   const int nv = F >> 2;  // float4 per row
   for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < n;
@@ -99,10 +98,17 @@ __global__ void __launch_bounds__(256) k_spmm_rows_v4(int64_t n, int32_t F, cons
     for (int q = 0; q < FV; ++q)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[q][c] = 0.0;
+    // (column, weight) of the next 32 nonzeros are loaded while this chunk's rows are summed
+    int64_t jn = b + lane < e ? col[b + lane] : 0;
+    double wn = b + lane < e ? val[b + lane] : 0.0;
     for (int64_t p0 = b; p0 < e; p0 += 32) {
       const int m = static_cast<int>(min(static_cast<int64_t>(32), e - p0));
-      const int64_t jl = lane < m ? col[p0 + lane] : 0;
-      const double wl = lane < m ? val[p0 + lane] : 0.0;
+      const int64_t jl = jn;
+      const double wl = wn;
+      if (p0 + 32 < e) {
+        jn = p0 + 32 + lane < e ? col[p0 + 32 + lane] : 0;
+        wn = p0 + 32 + lane < e ? val[p0 + 32 + lane] : 0.0;
+      }
       for (int s0 = 0; s0 < m; s0 += kAhead) {
         float4 xv[kAhead][FV];
         double w[kAhead];
@@ -156,8 +162,11 @@ cudaError_t launch_spmm(int64_t n, int32_t F, const int64_t* row_ptr, const int6
   const int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, 148ll * 64);
   const bool vec = F % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
                    !(getenv("PPLOAD_SPMM") && !strcmp(getenv("PPLOAD_SPMM"), "scalar"));
-  if (vec && F <= 128) k_spmm_rows_v4<1><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
-  else if (vec && F <= 256) k_spmm_rows_v4<2><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  const int ahead = getenv("PPLOAD_SPMM_AHEAD") ? atoi(getenv("PPLOAD_SPMM_AHEAD")) : 4;  // r1m: 8 is slower (registers)
+  const uint32_t g = static_cast<uint32_t>(blocks);
+  if (vec && F <= 128 && ahead == 4) k_spmm_rows_v4<1, 4><<<g, 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  else if (vec && F <= 128) k_spmm_rows_v4<1, 8><<<g, 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
+  else if (vec && F <= 256) k_spmm_rows_v4<2, 4><<<g, 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 32) k_spmm_rows<1><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 64) k_spmm_rows<2><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
   else if (F <= 128) k_spmm_rows<4><<<static_cast<uint32_t>(blocks), 256, 0, st>>>(n, F, row_ptr, col, val, x, y);
