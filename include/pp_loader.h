@@ -238,6 +238,38 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
 pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col_idx, const float* X,
                        int32_t K, float* hops, void* stream);
 
+/* Pre-propagation INTO the loader's store, one hop per call (SURVEY.md
+ * §8(f)-2, the multi-GPU 1D-partitioned SpMM; Eq. (2), PAPER.md:158-167,
+ * operator PAPER.md:182): for every node i this rank owns (local row lr,
+ * global id i = lr*W + rank)
+ *   store[lr][k][:] = sum_{j in row i, ascending j} w_ij * X_{k-1}[j][:],
+ *   w_ij = 1/sqrt(d~_i d~_j),
+ * where X_{k-1}[j] is hop slot k-1 of node j's record in its OWNER's store
+ * (owner j mod W, local row j div W): local HBM, the pinned spill, or a peer's
+ * HBM over NVLink (PP_PEERS_IPC / PP_PEERS_LOOPBACK, after linking).  Same
+ * arithmetic as pp_propagate: bit-identical to the CPU reference definition.
+ * So hop 0 (X) given at create -- e.g. hop_stride = 0 with data = X broadcasts
+ * X into every slot -- plus K calls k = 1..K turn the store into the
+ * pre-propagated input without a hop-major copy of the K+1 matrices.  When the
+ * rank keeps an exchange copy (pp_loader_info.exchange_cast) its slot k is
+ * rewritten with the cast in the same kernel.
+ *   k:       hop slot to write, 1 <= k < H (slot k-1 is read).
+ *   row_ptr: device int64 [local_rows + 1], col_idx: device int64 [nnz]:
+ *            the CSR rows of A~ = I + A for this rank's nodes in local-row
+ *            order, GLOBAL column ids ascending within a row, each row
+ *            holding its diagonal entry.
+ *   deg:     device int32 [N_total]: d~_j (row length of A~) of every node;
+ *            deg[i] must equal the length of i's row here.
+ * Requires an fp32 store, F <= 256.  Enqueued on `stream`, ordered after the
+ * loader's earlier work, and the loader's later work is ordered after it.
+ * W > 1: hop k reads every owner's slot k-1, so all ranks must have finished
+ * hop k-1 first (the caller synchronises `stream` and barriers between hops;
+ * loopback shards sharing one `stream` are ordered by it).
+ * Errors: PP_ERR_INVALID (k, dtype, F, NULL pointers), PP_ERR_STATE (not
+ * linked), PP_ERR_CUDA. */
+pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, const int64_t* col_idx,
+                             const int32_t* deg, void* stream);
+
 /* Move the cursor to step t (0 <= t <= steps_per_epoch): resume support.
  * (seed, chunk, cursor) is the loader's whole epoch state. */
 pp_status pp_seek(pp_loader* L, int64_t step);

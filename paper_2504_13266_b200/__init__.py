@@ -27,7 +27,7 @@ __all__ = [
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
     "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
-    "pp_epoch_permute_local",
+    "pp_epoch_permute_local", "pp_propagate_store",
 ]
 
 
@@ -178,6 +178,13 @@ def pp_propagate(row_ptr, col_idx, X, K, hops, stream=None) -> None:
            "pp_propagate")
 
 
+def pp_propagate_store(h, k: int, row_ptr, col_idx, deg, stream=None) -> None:
+    """Hop slot k of this rank's store records = B (slot k-1 of every owner's records): device int64
+    local CSR (global columns), device int32 global degrees d~."""
+    _check(lib().pp_propagate_store(h, k, _ptr(row_ptr), _ptr(col_idx), _ptr(deg), _stream(stream)),
+           "pp_propagate_store")
+
+
 def pp_seek(h, step: int) -> None:
     _check(lib().pp_seek(h, step), "pp_seek")
 
@@ -274,6 +281,9 @@ class Loader:
 
     def next_batches_linear(self, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream=None):
         return pp_next_batches_linear(self.h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream)
+
+    def propagate_store(self, k, row_ptr, col_idx, deg, stream=None):
+        pp_propagate_store(self.h, k, row_ptr, col_idx, deg, stream)
 
     def seek(self, step):
         pp_seek(self.h, step)

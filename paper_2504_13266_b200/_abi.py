@@ -19,7 +19,7 @@ EXPORTS = [
     "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
     "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
-    "pp_epoch_permute_local",
+    "pp_epoch_permute_local", "pp_propagate_store",
 ]
 
 
@@ -117,6 +117,7 @@ def lib():
                 "pp_next_batches_linear": (st, [P, i32, P, i32, P, ctypes.c_int, i64, P, P, P]),
                 "pp_propagate": (st, [i64, i32, P, P, P, i32, P, P]),
                 "pp_epoch_permute_local": (st, [P, u64, i64, P]),
+                "pp_propagate_store": (st, [P, i32, P, P, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

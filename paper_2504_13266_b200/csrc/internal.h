@@ -125,6 +125,21 @@ cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int6
                                    cudaStream_t st);
 cudaError_t launch_spmm(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col, const double* val,
                         const float* x, float* y, cudaStream_t st);
+// Propagation into the loader's node-major fp32 store (pp_propagate_store).
+struct StorePropArgs {
+  int64_t local_rows;       // rows of this rank (CSR rows, local order)
+  int32_t F, k;             // features; hop slot written (reads slot k-1)
+  int32_t W, rank;
+  const int64_t* row_ptr;   // [local_rows + 1]
+  const int64_t* col;       // global column ids
+  const int32_t* deg;       // [N_total] d~ (row lengths of I + A)
+  ShardView shards[kMaxWorld];  // fp32 stores of every owner (shards[rank] = own)
+  int64_t rec_stride;
+  uint8_t* xstore;          // own exchange copy or null: slot k rewritten with the cast
+  int64_t xrec_stride;
+  int32_t x_dtype;          // 1 bf16, 2 f16
+};
+cudaError_t launch_spmm_store(const StorePropArgs& a, cudaStream_t st);
 
 // ---- exchange copy (gather.cu) ----------------------------------------------
 // dst[r] = cast(src[r]) for rows [0, rows): fp32 records (pitch rec_stride) ->

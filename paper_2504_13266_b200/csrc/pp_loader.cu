@@ -443,6 +443,44 @@ pp_status pp_loader_destroy(pp_loader* L) {
   return PP_OK;
 }
 
+pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, const int64_t* col_idx,
+                             const int32_t* deg, void* stream) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
+  if (!row_ptr || !col_idx || !deg) return fail(PP_ERR_INVALID, "NULL CSR / degree pointer");
+  if (L->in_dtype != PP_F32) return fail(PP_ERR_INVALID, "pp_propagate_store needs an fp32 store");
+  if (k < 1 || k >= L->H) return fail(PP_ERR_INVALID, "hop slot k = %d must be in [1, H-1 = %d]", k, L->H - 1);
+  if (L->F > 256) return fail(PP_ERR_INVALID, "F = %d > 256", L->F);
+  if (!L->linked) return fail(PP_ERR_STATE, "sharded loader not linked to its peers yet");
+  DevGuard g(L->dev);
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  if (user != L->stream) {  // order after this loader's gathers (they read the store) ...
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, L->stream));
+    PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_in, 0));
+  }
+  StorePropArgs a{};
+  a.local_rows = L->local_rows;
+  a.F = L->F;
+  a.k = k;
+  a.W = L->W;
+  a.rank = L->rank;
+  a.row_ptr = row_ptr;
+  a.col = col_idx;
+  a.deg = deg;
+  for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = L->shards[i];
+  a.rec_stride = L->rec_stride;
+  a.xstore = L->d_xstore;
+  a.xrec_stride = L->xrec_stride;
+  a.x_dtype = L->out_dtype == PP_F16 ? 2 : 1;
+  PPL_CUDA(L, launch_spmm_store(a, user));
+  if (user != L->stream) {  // ... and later loader work after this hop
+    PPL_CUDA(L, cudaEventRecord(L->ev_out, user));
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_out, 0));
+  }
+  L->last_was_gather = false;
+  return PP_OK;
+}
+
 pp_status pp_set_stream(pp_loader* L, void* stream) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
@@ -473,7 +511,6 @@ static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint3
   } else {
     if (L->pi_cap < U) {
       cudaFree(L->d_pi);
-  cudaFree(L->d_wimg);
       L->d_pi = nullptr;
       if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
       L->pi_cap = U;

@@ -52,3 +52,31 @@ peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEAS
 print(json.dumps({"config": "products-sized ER graph", "n": n, "nnz": nnz, "F": F, "K": K, "ms": ms,
                   "algorithmic_GBs": total / ms / 1e6, "frac_hbm": total / ms / 1e6 / peak,
                   "ms_per_hop": ms / K}))
+
+# Same graph, propagated INTO a loader store (pp_propagate_store: node-major [n, K+1, F] fp32
+# records, hop slot k from slot k-1, weights from the degree array on the fly).
+del hops
+deg = torch.diff(row_ptr).to(torch.int32)
+L = pp.Loader(data=X, where=pp.PP_MEM_DEVICE, num_nodes=n, num_hops=K + 1, feat_dim=F, hop_stride=0, row_stride=F,
+              dtype=pp.PP_F32, batch_size=8192, out_dtype=pp.PP_BF16)
+s = torch.cuda.current_stream()
+
+
+def store_pass():
+    for k in range(1, K + 1):
+        L.propagate_store(k, row_ptr, col, deg, s)
+
+
+store_pass()
+torch.cuda.synchronize()
+a.record()
+for _ in range(reps):
+    store_pass()
+b.record()
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / reps
+per_hop = nnz * (F * 4 + 8 + 4) + n * (F * 4 + 16)
+print(json.dumps({"config": "products-sized ER graph, into the loader store", "kernel": "k_spmm_store_v4", "n": n,
+                  "nnz": nnz, "F": F, "K": K, "ms": ms, "algorithmic_GBs": K * per_hop / ms / 1e6,
+                  "frac_hbm": K * per_hop / ms / 1e6 / peak, "ms_per_hop": ms / K}))
+L.close()
