@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 2
+#define PP_ABI_VERSION 3
 
 /* Bytes of one rank's exported store handle (pp_export_store). */
 #define PP_IPC_HANDLE_BYTES 128
@@ -66,7 +66,8 @@ typedef enum {
 } pp_status;
 
 typedef enum { PP_F32 = 0, PP_BF16 = 1, PP_F16 = 2 } pp_dtype;
-typedef enum { PP_MEM_HOST = 0, PP_MEM_DEVICE = 1 } pp_mem;
+/* PP_MEM_FILES: the storage tier (see pp_hop_desc). */
+typedef enum { PP_MEM_HOST = 0, PP_MEM_DEVICE = 1, PP_MEM_FILES = 2 } pp_mem;
 
 /* How the W ranks of a sharded loader reach each other's stores. */
 typedef enum {
@@ -83,7 +84,23 @@ typedef enum {
  *   node-major [N][H][F]: hop_stride = F,   row_stride = H*F
  * Requirements: row_stride >= F.  data == NULL: allocate the store only
  * (fill it with pp_fill_synthetic).  For W > 1, data (if given) covers all
- * N rows; rank r copies only the rows it owns (v mod W == r). */
+ * N rows; rank r copies only the rows it owns (v mod W == r).
+ *
+ * where == PP_MEM_FILES (storage tier; "Direct Storage
+ * Access"): data is a `const char* const*` array of H file
+ * paths, hop k's file holding X_k as raw little-endian [N_total][F] of dtype
+ * (no header; "we split input features of different hops into separate
+ * files"); hop_stride / row_stride are ignored.  No store is
+ * built: every step's rows are read from the files (one read per run of
+ * consecutive node ids and hop -- a chunk with chunk reshuffling
+ * -- O_DIRECT unless the file system refuses it or PPLOAD_IO_DIRECT=0) into a
+ * pinned staging slot by a pool of I/O threads, DMA'd to the GPU and cast into
+ * `out` there; the next step is read while the GPU consumes the current one.
+ * The files must stay unchanged while the loader lives.  W > 1 is allowed with
+ * peers == PP_PEERS_NONE: each rank reads its own slice of the global epoch
+ * from the shared files.  Not available for file loaders: a store (so no
+ * pp_fill_synthetic / pp_read_store / pp_propagate_store / fused linear /
+ * peer linking), pp_epoch_permute_local, hbm_budget_bytes. */
 typedef struct {
   const void* data;
   pp_mem where;        /* memory space of data */
@@ -112,7 +129,8 @@ typedef struct {
                                placement).  W > 1 requires no spill. */
   int32_t world_size;       /* W >= 1 */
   int32_t rank;             /* 0 <= r < W */
-  pp_peers peers;           /* PP_PEERS_NONE iff W == 1 */
+  pp_peers peers;           /* PP_PEERS_NONE iff W == 1 (file loaders: always
+                               PP_PEERS_NONE, any W) */
   int32_t device;           /* CUDA device ordinal */
 } pp_loader_desc;
 
@@ -134,7 +152,8 @@ typedef struct {
   int64_t epoch_positions;  /* positions of the current epoch (N, or local_rows when local) */
   int32_t exchange_cast;    /* 1: this rank keeps a cast exchange copy of its HBM rows that the
                                peers read instead of the fp32 records (W > 1, see below) */
-  int32_t reserved0;
+  int32_t storage_mode;     /* 0: no file tier; 1: file tier with O_DIRECT reads; 2: buffered reads */
+  int64_t storage_bytes_read; /* bytes read from the hop files so far (aligned extents included) */
 } pp_loader_info;
 
 /* Create a loader.  Copies the hop data into a library-owned, node-major store

@@ -17,7 +17,7 @@ import numpy as np
 
 from ._abi import (  # noqa: F401
     PP_OK, PP_ERR_INVALID, PP_ERR_OOM, PP_ERR_CUDA, PP_ERR_NCCL, PP_ERR_STATE, PP_END_OF_EPOCH,
-    PP_F32, PP_BF16, PP_F16, PP_MEM_HOST, PP_MEM_DEVICE, PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK,
+    PP_F32, PP_BF16, PP_F16, PP_MEM_HOST, PP_MEM_DEVICE, PP_MEM_FILES, PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK,
     pp_hop_desc, pp_loader_desc, pp_loader_info, PPError, lib, LIB_PATH,
 )
 
@@ -82,12 +82,18 @@ def pp_footprint_bytes(num_nodes, feat_dim, elem_bytes, num_ops, num_hops_R) -> 
 
 def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_dim, hop_stride=0, row_stride=0,
                      dtype=PP_F32, node_set=None, labels=None, batch_size, out_dtype=PP_BF16, drop_last=False,
-                     hbm_budget_bytes=0, world_size=1, rank=0, peers=PP_PEERS_NONE, device=0):
+                     hbm_budget_bytes=0, world_size=1, rank=0, peers=PP_PEERS_NONE, device=0, files=None):
     """pp_loader_create(desc) -> handle.  ``data`` is a numpy array (host) or a torch CUDA tensor
-    (device) of the hop matrices with the given element strides; None allocates the store only."""
+    (device) of the hop matrices with the given element strides; None allocates the store only.
+    ``files``: H hop file paths (raw [N][F] of dtype each) -> the storage tier (PP_MEM_FILES)."""
     d = pp_loader_desc()
     keep = []
-    if data is not None:
+    if files is not None:
+        paths = (ctypes.c_char_p * len(files))(*[os.fsencode(f) for f in files])
+        keep.append(paths)
+        d.hops.data = ctypes.cast(paths, ctypes.c_void_p).value
+        where = PP_MEM_FILES
+    elif data is not None:
         if isinstance(data, np.ndarray):
             data = np.ascontiguousarray(data)
             keep.append(data)

@@ -10,7 +10,7 @@ LIB_PATH = os.path.join(HERE, "libppload.so")
 
 PP_OK, PP_ERR_INVALID, PP_ERR_OOM, PP_ERR_CUDA, PP_ERR_NCCL, PP_ERR_STATE, PP_END_OF_EPOCH = range(7)
 PP_F32, PP_BF16, PP_F16 = 0, 1, 2
-PP_MEM_HOST, PP_MEM_DEVICE = 0, 1
+PP_MEM_HOST, PP_MEM_DEVICE, PP_MEM_FILES = 0, 1, 2
 PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK = 0, 1, 2
 
 # every symbol include/pp_loader.h declares (checked by tests/test_abi.py)
@@ -76,7 +76,8 @@ class pp_loader_info(ctypes.Structure):
         ("local_epoch", ctypes.c_int32),
         ("epoch_positions", ctypes.c_int64),
         ("exchange_cast", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("storage_mode", ctypes.c_int32),
+        ("storage_bytes_read", ctypes.c_int64),
     ]
 
 

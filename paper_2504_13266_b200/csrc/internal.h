@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 namespace ppl {
 
@@ -151,6 +152,24 @@ cudaError_t launch_cast_records(const uint8_t* src, int64_t rows, int64_t rec_st
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
                                   int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,
                                   cudaStream_t st);
+
+// ---- storage tier (storage.cu) ----------------------------------------------
+struct FileTier;
+FileTier* file_tier_open(const char* const* paths, int H, int64_t N_total, int F, int s_in, int64_t B, int dev,
+                         std::string* err);
+void file_tier_close(FileTier* T);
+bool file_tier_direct(const FileTier* T);
+int64_t file_tier_bytes_read(const FileTier* T);
+void file_tier_reset(FileTier* T);  // drop staged steps (waits for their reads)
+// New epoch: host order (N positions -> node-set index or node id), optional host
+// node set, slicing (B from open, W, rank) and step count; grows the staging
+// for the epoch's largest step.  The arrays must live until the next call.
+bool file_tier_set_epoch(FileTier* T, uint64_t epoch, const uint32_t* order, const int64_t* node_set, int64_t N,
+                         int32_t W, int32_t rank, int64_t steps, std::string* err);
+// Assemble `step` into out on st (waits for its reads; keeps the next steps staging).
+cudaError_t file_tier_step(FileTier* T, int64_t step, int32_t in_dtype, int32_t out_dtype, const int32_t* labels,
+                           uint8_t* out, int32_t* out_labels, int64_t* out_nodes, cudaStream_t st, int32_t* rows,
+                           std::string* err);
 
 // order (u32 positions) -> global node ids (int64), for pp_get_order.
 cudaError_t launch_order_to_nodes(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t* dst,

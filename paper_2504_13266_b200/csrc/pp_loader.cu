@@ -109,6 +109,12 @@ struct pp_loader {
   bool linked = false;
   std::vector<void*> ipc_opened;
 
+  // storage tier (hops.where == PP_MEM_FILES): no store; steps are read from the hop files
+  FileTier* files = nullptr;
+  std::vector<uint32_t> h_order;      // host copy of the current epoch's order
+  std::vector<int64_t> h_node_set;    // host copy of the node set (empty: identity)
+  uint64_t epoch_id = 0;              // bumped by every permute / seek (invalidates staged steps)
+
   bool permuted = false, poisoned = false;
   bool local = false;         // current epoch from pp_epoch_permute_local
   int64_t steps_global = 0;   // steps of a global-permutation epoch
@@ -132,6 +138,7 @@ pp_status cuda_fail(pp_loader* L, cudaError_t e, const char* what) {
 void release(pp_loader* L) {
   if (!L) return;
   if (L->stream) cudaStreamSynchronize(L->stream);
+  if (L->files) file_tier_close(L->files);
   for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(L->d_store);
   cudaFree(L->d_xstore);
@@ -196,11 +203,15 @@ pp_status validate(const pp_loader_desc* d) {
   if (static_cast<int64_t>(h.num_hops) * h.feat_dim >= (int64_t(1) << 24))
     return fail(PP_ERR_INVALID, "H*F too large");
   if (!valid_dtype(h.dtype) || !valid_dtype(d->out_dtype)) return fail(PP_ERR_INVALID, "unknown dtype");
-  if (h.where != PP_MEM_HOST && h.where != PP_MEM_DEVICE) return fail(PP_ERR_INVALID, "unknown memory kind");
+  if (h.where != PP_MEM_HOST && h.where != PP_MEM_DEVICE && h.where != PP_MEM_FILES)
+    return fail(PP_ERR_INVALID, "unknown memory kind");
+  const bool files = h.where == PP_MEM_FILES;
+  if (files && !h.data) return fail(PP_ERR_INVALID, "PP_MEM_FILES needs the array of H hop file paths");
+  if (files && d->peers != PP_PEERS_NONE) return fail(PP_ERR_INVALID, "file loaders take peers = PP_PEERS_NONE");
   const bool cast = h.dtype == PP_F32 && (d->out_dtype == PP_BF16 || d->out_dtype == PP_F16);
   if (!cast && h.dtype != d->out_dtype)
     return fail(PP_ERR_INVALID, "unsupported dtype pair (store %d -> out %d)", h.dtype, d->out_dtype);
-  if (h.data) {
+  if (h.data && !files) {
     if (h.row_stride < h.feat_dim || h.hop_stride < 0)
       return fail(PP_ERR_INVALID, "row_stride must be >= feat_dim and hop_stride >= 0");
   }
@@ -208,7 +219,7 @@ pp_status validate(const pp_loader_desc* d) {
   if (d->world_size < 1 || d->world_size > kMaxWorld)
     return fail(PP_ERR_INVALID, "world_size must be in [1, %d]", kMaxWorld);
   if (d->rank < 0 || d->rank >= d->world_size) return fail(PP_ERR_INVALID, "rank out of range");
-  if ((d->world_size == 1) != (d->peers == PP_PEERS_NONE))
+  if (!files && (d->world_size == 1) != (d->peers == PP_PEERS_NONE))
     return fail(PP_ERR_INVALID, "peers must be PP_PEERS_NONE iff world_size == 1");
   if (d->peers != PP_PEERS_NONE && d->peers != PP_PEERS_IPC && d->peers != PP_PEERS_LOOPBACK)
     return fail(PP_ERR_INVALID, "unknown peers mode");
@@ -345,6 +356,15 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     return s;
   };
   cudaError_t e_x = cudaSuccess;
+  const bool files = desc->hops.where == PP_MEM_FILES;
+  if (files) {
+    std::string err;
+    L->files = file_tier_open(static_cast<const char* const*>(desc->hops.data), L->H, L->N_total, L->F,
+                              elem_bytes(L->in_dtype), L->B, L->dev, &err);
+    if (!L->files) return bail(fail(PP_ERR_INVALID, "storage tier: %s", err.c_str()));
+    L->h_order.resize(L->N);
+    if (desc->node_set) L->h_node_set.assign(desc->node_set, desc->node_set + L->N);
+  }
 
   // ---- placement: HBM budget, remainder spills to pinned mapped host memory
   const int64_t scratch = L->N * 4 * 3 + (int64_t(1) << 26) + (L->has_labels ? L->N_total * 4 : 0);
@@ -355,7 +375,8 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     budget = static_cast<int64_t>(fr) - (int64_t(2) << 30) - scratch - L->N_total * 4 - L->N * 8;
     if (budget < 0) budget = 0;
   }
-  L->n_hbm = budget < 0 ? 0 : std::min<int64_t>(L->local_rows, budget / L->rec_stride);
+  L->n_hbm = files ? 0 : budget < 0 ? 0 : std::min<int64_t>(L->local_rows, budget / L->rec_stride);
+  if (files) L->local_rows = 0;
   L->n_spill = L->local_rows - L->n_hbm;
   if (L->W > 1 && L->n_spill > 0 && desc->peers == PP_PEERS_IPC)
     return bail(fail(PP_ERR_INVALID, "sharded (IPC) loaders need the whole shard in HBM (%lld rows spill)",
@@ -370,7 +391,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->d_spill), L->h_spill, 0) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "cudaHostGetDevicePointer failed"));
   }
-  if (desc->hops.data) {
+  if (desc->hops.data && !files) {
     cudaError_t e = copy_in(L, desc->hops, 0, L->n_hbm, L->d_store);
     if (e == cudaSuccess && L->n_spill > 0) e = copy_in(L, desc->hops, L->n_hbm, L->n_spill, L->h_spill);
     if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
@@ -417,7 +438,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
-  L->linked = (L->W == 1);
+  L->linked = (L->W == 1) || files;
   // ---- exchange copy for the peers (see pp_loader.h): only if it fits after everything else
   if (L->W > 1 && L->in_dtype == PP_F32 && L->out_dtype != PP_F32 && L->vector_path) {
     L->xrec_stride = (L->rec_out + 15) / 16 * 16;
@@ -448,7 +469,7 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!row_ptr || !col_idx || !deg) return fail(PP_ERR_INVALID, "NULL CSR / degree pointer");
-  if (L->in_dtype != PP_F32) return fail(PP_ERR_INVALID, "pp_propagate_store needs an fp32 store");
+  if (L->in_dtype != PP_F32 || L->files) return fail(PP_ERR_INVALID, "pp_propagate_store needs an fp32 store");
   if (k < 1 || k >= L->H) return fail(PP_ERR_INVALID, "hop slot k = %d must be in [1, H-1 = %d]", k, L->H - 1);
   if (L->F > 256) return fail(PP_ERR_INVALID, "F = %d > 256", L->F);
   if (!L->linked) return fail(PP_ERR_STATE, "sharded loader not linked to its peers yet");
@@ -530,6 +551,7 @@ pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, voi
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (L->d_node_set) return fail(PP_ERR_INVALID, "local shuffling is defined without a node set");
+  if (L->files) return fail(PP_ERR_INVALID, "file loaders have no local shard to shuffle");
   if (chunk < 1 || chunk > L->local_rows)
     return fail(PP_ERR_INVALID, "chunk must be in [1, local_rows=%lld]", (long long)L->local_rows);
   DevGuard g(L->dev);
@@ -588,6 +610,18 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
   }
+  if (L->files) {  // the I/O planner needs the order on the host
+    file_tier_reset(L->files);
+    PPL_CUDA(L, cudaMemcpyAsync(L->h_order.data(), L->d_order, L->N * 4, cudaMemcpyDeviceToHost, L->stream));
+    PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+    ++L->epoch_id;
+    std::string err;
+    if (!file_tier_set_epoch(L->files, L->epoch_id, L->h_order.data(), L->h_node_set.empty() ? nullptr : L->h_node_set.data(),
+                             L->N, L->W, L->rank, L->steps_global, &err)) {
+      L->poisoned = true;
+      return fail(PP_ERR_OOM, "storage tier: %s", err.c_str());
+    }
+  }
   L->local = false;
   L->steps = L->steps_global;
   L->last_was_gather = false;
@@ -645,6 +679,28 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
     PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
     L->last_was_gather = false;
+  }
+  if (L->files) {
+    // storage tier: each step's rows are read from the hop files, then assembled on the GPU
+    for (int64_t i = 0; i < nsteps; ++i) {
+      std::string err;
+      cudaError_t e = file_tier_step(L->files, L->cursor + i, L->in_dtype, L->out_dtype, L->d_labels,
+                                     static_cast<uint8_t*>(out) + i * out_stride, out_labels ? out_labels + i * L->B : nullptr,
+                                     out_nodes ? out_nodes + i * L->B : nullptr, L->stream, &rows[i], &err);
+      if (e == cudaErrorUnknown) {
+        L->poisoned = true;
+        return fail(PP_ERR_CUDA, "storage tier: %s", err.c_str());
+      }
+      if (e != cudaSuccess) return cuda_fail(L, e, "storage tier step");
+    }
+    if (handoff) {
+      PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+      PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
+    }
+    L->last_was_gather = false;
+    L->cursor += nsteps;
+    if (n_done) *n_done = static_cast<int32_t>(nsteps);
+    return PP_OK;
   }
   GatherArgs a{};
   a.order = L->d_order;
@@ -709,7 +765,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1 || !W || !Z) return fail(PP_ERR_INVALID, "NULL argument or n < 1");
-  if (L->in_dtype != PP_F32 || L->n_spill > 0 || L->W != 1)
+  if (L->in_dtype != PP_F32 || L->n_spill > 0 || L->W != 1 || L->files)
     return fail(PP_ERR_INVALID, "fused linear needs an fp32, HBM-resident, unsharded store");
   if (!linear_supported(L->H, L->F, D, L->num_sms))
     return fail(PP_ERR_INVALID, "fused linear supports F <= 128 with F %% 4 == 0 and D in {256, 512} (F=%d, D=%d)",
@@ -813,6 +869,7 @@ pp_status pp_seek(pp_loader* L, int64_t step) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (!L->permuted) return fail(PP_ERR_STATE, "pp_seek before pp_epoch_permute");
   if (step < 0 || step > L->steps) return fail(PP_ERR_INVALID, "step out of range");
+  if (L->files && step != L->cursor) file_tier_reset(L->files);  // staged next step no longer follows
   L->cursor = step;
   return PP_OK;
 }
@@ -834,7 +891,8 @@ pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
   info->local_epoch = L->local ? 1 : 0;
   info->epoch_positions = L->local ? L->local_rows : L->N;
   info->exchange_cast = L->d_xstore != nullptr ? 1 : 0;
-  info->reserved0 = 0;
+  info->storage_mode = L->files ? (file_tier_direct(L->files) ? 1 : 2) : 0;
+  info->storage_bytes_read = L->files ? file_tier_bytes_read(L->files) : 0;
   return PP_OK;
 }
 
@@ -842,6 +900,7 @@ pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (L->in_dtype == PP_BF16) return fail(PP_ERR_INVALID, "no synthetic generator for bf16 stores");
+  if (L->files) return fail(PP_ERR_INVALID, "file loaders have no store to fill");
   DevGuard g(L->dev);
   PPL_CUDA(L, launch_fill_synthetic(L->d_store, 0, L->n_hbm, L->rec_stride, L->H, L->F, L->in_dtype, data_seed, L->W,
                                     L->rank, L->stream));
@@ -871,6 +930,7 @@ pp_status pp_get_order(pp_loader* L, int64_t* dst_host) {
 pp_status pp_read_store(pp_loader* L, int64_t row0, int64_t n, void* dst_host) {
   if (!L || !dst_host) return fail(PP_ERR_INVALID, "NULL argument");
   if (row0 < 0 || n < 0 || row0 + n > L->local_rows) return fail(PP_ERR_INVALID, "row range out of bounds");
+  if (L->files) return fail(PP_ERR_INVALID, "file loaders have no store");
   DevGuard g(L->dev);
   PPL_CUDA(L, cudaStreamSynchronize(L->stream));
   uint8_t* dst = static_cast<uint8_t*>(dst_host);
