@@ -358,7 +358,7 @@ def consumer_fused_linear(pp, torch, cfg, args, D=512, k=8, reps=5):
     steps = L.query()["steps_per_epoch"]
     W = torch.from_numpy((np.random.default_rng(0).standard_normal((H, F, D)) / 10).astype(np.float32)).cuda()
     W = W.to(torch.bfloat16)
-    nslots = 16
+    nslots = steps  # one Z slot per step (10 GB): back-to-back launches may overlap (PDL)
     Z = torch.empty((nslots, B, H, D), dtype=torch.bfloat16, device="cuda")
     zs = B * H * D * 2
 

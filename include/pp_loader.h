@@ -234,7 +234,12 @@ pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride
  *      F <= 128, F % 4 == 0, and W == 1.
  *   Z: device [n][B][H][D] of z_dtype (PP_BF16: RNE from fp32, or PP_F32),
  *      slot pitch z_stride_bytes (>= B*H*D*elem when n > 1), 16-B aligned.
- * Cursor, rows[], n_done and stream semantics as pp_next_batches.
+ * W is read by TMA at every launch (nothing is cached across calls), so it may
+ * change between calls (an optimizer step).
+ * Cursor, rows[], n_done and stream semantics as pp_next_batches; in
+ * particular, calls issued back to back with consumer_stream == the loader
+ * stream may overlap (programmatic dependent launch), so give each such call
+ * its own Z slots or put the work that consumes / rewrites them between calls.
  * Errors: PP_ERR_INVALID (unsupported loader or shapes), PP_ERR_STATE,
  * PP_END_OF_EPOCH, PP_ERR_CUDA. */
 pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,

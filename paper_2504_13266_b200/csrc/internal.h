@@ -102,8 +102,7 @@ struct LinearArgs {
   int64_t rec_stride;
   int64_t N, first_pos, step_stride;
   int32_t B, nsteps;
-  const void* W;            // bf16 [H][F][D]
-  uint8_t* w_img;           // [H][2 K blocks][D rows][128 B] scratch: W_k^T in the UMMA layout
+  const void* W;            // bf16 [H][F][D], read by TMA (MN-major B operand)
   int32_t H, F, D;
   uint8_t* Z;               // [nsteps][B][H][D] of z_elem bytes
   int64_t z_stride;         // bytes between step slots
@@ -117,9 +116,11 @@ struct LinearArgs {
   uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null
 };
 bool linear_supported(int H, int F, int D, int num_sms);
-size_t linear_w_image_bytes(int H, int D);
-// Launches the W-image kernel, then the fused kernel, both on `st`.
-cudaError_t launch_gather_linear(const LinearArgs& a, cudaStream_t st);
+// Encodes the Z and W tensor maps and launches the fused kernel on `st`.
+// pdl: programmatic dependent launch (only right after another fused launch of this
+// epoch on `st`: launches are independent, so the next grid's CTAs may start on SMs
+// the previous grid's finished CTAs have left).
+cudaError_t launch_gather_linear(const LinearArgs& a, bool pdl, cudaStream_t st);
 
 // ---- Eq. (2) propagation (propagate.cu) --------------------------------------
 cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int64_t* col, double* val,

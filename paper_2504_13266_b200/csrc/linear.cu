@@ -7,9 +7,10 @@
 // to the batch the loader assembles, without the batch ever landing in HBM.
 //
 // B200 design (one persistent CTA per SM, 12 warps, 1 CTA/SM by shared memory):
-//   * CTA (k, q): hop k = blockIdx % H; it keeps W_k^T resident in shared memory
-//     (K-major, 128-byte swizzle, zero-padded to K = 128) and walks M-tiles of
-//     128 batch rows q, q + Q, ...
+//   * CTA (k, q): hop k = blockIdx % H; it keeps W_k resident in shared memory,
+//     loaded by TMA straight from the caller's [F][D] tensor as the MN-major
+//     SWIZZLE_128B B operand (64-column boxes of 128 K rows, rows >= F zero-filled
+//     by the TMA out-of-bounds fill), and walks M-tiles of 128 batch rows q, q + Q, ...
 //   * warps 0-3 (producers): thread r resolves batch row r (order -> node set ->
 //     record), loads its hop-k fp32 vector with 128-bit loads, converts with
 //     cvt.rn.bf16x2.f32 (the loader's RNE cast) and writes the 128 x 128 bf16 A
@@ -47,10 +48,16 @@ constexpr int kTileM = 128;        // batch rows per tile (UMMA M)
 constexpr int kUmmaN = 256;        // columns per accumulator (UMMA N)
 constexpr int kKPad = 128;         // F zero-padded to two 64-element K blocks
 constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
-constexpr int kStages = 2;
+#ifndef PPL_LIN_STAGES
+#define PPL_LIN_STAGES 2
+#endif
+#ifndef PPL_LIN_EPIBUFS
+#define PPL_LIN_EPIBUFS 2
+#endif
+constexpr int kStages = PPL_LIN_STAGES;  // A-tile stages
 constexpr int kStageBytes = 32 * 128;  // epilogue staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
-constexpr int kEpiBufs = 2;         // staging buffers per epilogue warp
-constexpr int kWCopyChunk = 16384;  // bytes per bulk copy of the W image
+constexpr int kEpiBufs = PPL_LIN_EPIBUFS;  // staging buffers per epilogue warp
+constexpr int kWBox = kKPad * 128;  // one TMA box of W_k: 128 K rows x 64 columns (128 B)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -100,10 +107,19 @@ __device__ __forceinline__ uint64_t sw128_desc(const void* p) {
          (1ull << 46) | (2ull << 61);
 }
 
+// B operand, MN-major SWIZZLE_128B: canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in
+// 16-byte units -- 64 consecutive columns per 128-byte row, one row per K index,
+// LBO = 16 KB between 64-column boxes, SBO = 1024 B between 8-row K groups.
+__device__ __forceinline__ uint64_t sw128_mn_desc(const void* p) {
+  return static_cast<uint64_t>((smem_addr(p) >> 4) & 0x3FFFu) | (static_cast<uint64_t>(kWBox >> 4) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
 // Instruction descriptor, kind::f16: D = F32 (bits 4-5 = 1), A = B = BF16 (bits
-// 7-9, 10-12 = 1), both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kUmmaN >> 3) << 17) |
-                            (static_cast<uint32_t>(kTileM >> 4) << 24);
+// 7-9, 10-12 = 1), A K-major, B MN-major (bit 16), N >> 3 at bits 17-22, M >> 4
+// at bits 24-28.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                            (static_cast<uint32_t>(kUmmaN >> 3) << 17) | (static_cast<uint32_t>(kTileM >> 4) << 24);
 
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
@@ -147,13 +163,17 @@ __device__ __forceinline__ void dbg_ts(const LinearArgs& a, int tile, int slot, 
 }  // namespace
 
 __global__ void __launch_bounds__(kLinThreads, 1)
-    k_gather_linear(const LinearArgs a, const __grid_constant__ CUtensorMap zmap) {
+    k_gather_linear(const LinearArgs a, const __grid_constant__ CUtensorMap zmap,
+                    const __grid_constant__ CUtensorMap wmap) {
   extern __shared__ uint8_t smem_raw[];
+  // consecutive fused launches of one epoch are independent: let the next one's CTAs
+  // take SMs as soon as this grid's CTAs leave them (see launch_gather_linear)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   dbg_cta(a, 0);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int D = a.D;
-  uint8_t* w_s = smem;                                // [2 kb][D rows][128 B]
-  uint8_t* a_s = smem + 2 * D * 128;                  // [kStages][2 kb][128 rows][128 B]
+  uint8_t* w_s = smem;                                // [D / 64 boxes][128 K rows][128 B]
+  uint8_t* a_s = smem + (D / 64) * kWBox;            // [kStages][2 kb][128 rows][128 B]
   uint8_t* z_s = a_s + kStages * kABytes;             // [epilogue warps][kEpiBufs][32 rows][128 B] staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * kEpiBufs * kStageBytes);
   uint64_t* a_full = bars;                            // [kStages], kProducerThreads arrivals
@@ -185,19 +205,20 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // W_k^T into shared memory: one bulk copy of the hop's pre-swizzled image
-  // (k_w_image), completed on w_full; only the MMA issuer waits for it, so the
-  // producers start gathering at once.
+  // W_k into shared memory: D / 64 TMA boxes straight from the caller's tensor
+  // (MN-major B operand; K rows >= F are zero-filled out of bounds), completed on
+  // w_full; only the MMA issuer waits for it, so the producers start gathering at once.
   if (threadIdx.x == 0) {
-    const uint32_t bytes = static_cast<uint32_t>(2 * D * 128);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(w_full)), "r"(bytes)
+    const uint32_t nbox = static_cast<uint32_t>(D / 64);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(w_full)),
+                 "r"(nbox * kWBox)
                  : "memory");
-    const uint8_t* src = a.w_img + static_cast<int64_t>(k) * bytes;
-    for (uint32_t off = 0; off < bytes; off += kWCopyChunk)
+    const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
+    for (uint32_t b = 0; b < nbox; ++b)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(w_s + off)),
-          "l"(src + off), "r"(kWCopyChunk), "r"(smem_addr(w_full))
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(smem_addr(w_s + b * kWBox)),
+          "l"(wmap_addr), "r"(static_cast<int>(b * 64)), "r"(0), "r"(k), "r"(smem_addr(w_full))
           : "memory");
   }
   dbg_cta(a, 1);
@@ -272,9 +293,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     };
     const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0;
     auto store_tile = [&](int i, const uint4(&x)[16]) {
-      const int s = i & 1;
+      const int s = i % kStages;
       if (dbg_lane) dbg_ts(a, i, 0, 0);
-      bar_wait(&a_empty[s], ((i >> 1) & 1) ^ 1);
+      bar_wait(&a_empty[s], ((i / kStages) & 1) ^ 1);
       if (dbg_lane) dbg_ts(a, i, 1, 0);
       uint8_t* at = a_s + s * kABytes;
 #pragma unroll
@@ -324,9 +345,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         int64_t step, pos;
         int r0;
         if (tile_rows(t, step, r0, pos) <= 0) continue;
-        const int s = i & 1;
+        const int s = i % kStages;
         const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0;
-        bar_wait(&a_full[s], (i >> 1) & 1);
+        bar_wait(&a_full[s], (i / kStages) & 1);
         tc_fence_after();
         if (dbg_lane) dbg_ts(a, i, 3, 0);
         const uint8_t* at = a_s + s * kABytes;
@@ -338,7 +359,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           for (int ks = 0; ks < ((a.debug & 64) ? 0 : kKPad / 16); ++ks) {
             const int kb = ks >> 2, j = ks & 3;
             const uint64_t ad = sw128_desc(at + kb * (kTileM * 128)) + 2 * j;  // +32 B per 16-element step
-            const uint64_t bd = sw128_desc(w_s + kb * D * 128 + h * kUmmaN * 128) + 2 * j;
+            const uint64_t bd = sw128_mn_desc(w_s + h * (kUmmaN / 64) * kWBox + ks * 2048);  // 16 K rows per step
             umma(tmem + h * kUmmaN, ad, bd, ks > 0 ? 1u : 0u);
           }
           umma_commit(&t_full[h]);
@@ -446,32 +467,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   dbg_cta(a, 3);
 }
 
-// W image: img[k][kb][n][chunk] = the 16-byte chunk of K-major row n (output
-// column d = n) holding K elements f = 64 kb + 8 c .. + 7 (zero for f >= F),
-// stored at chunk position c ^ (n & 7) (SWIZZLE_128B) -- the byte image the
-// fused kernel's B descriptors expect, so the CTA copies it verbatim.
-__global__ void k_w_image(const uint16_t* __restrict__ W, int H, int F, int D, uint8_t* __restrict__ img) {
-  const int64_t total = static_cast<int64_t>(H) * 2 * D * 8;  // 16-byte chunks
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i & 7), n = static_cast<int>((i >> 3) % D);
-    const int kb = static_cast<int>((i >> 3) / D % 2), k = static_cast<int>((i >> 3) / D / 2);
-    uint16_t v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int f = kb * 64 + c * 8 + j;
-      v[j] = f < F ? W[(static_cast<int64_t>(k) * F + f) * D + n] : static_cast<uint16_t>(0);
-    }
-    uint8_t* dst = img + ((static_cast<int64_t>(k) * 2 + kb) * D + n) * 128 + ((c ^ (n & 7)) << 4);
-    *reinterpret_cast<uint4*>(dst) = make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16),
-                                                v[4] | (uint32_t(v[5]) << 16), v[6] | (uint32_t(v[7]) << 16));
-  }
-}
-
-size_t linear_w_image_bytes(int H, int D) { return static_cast<size_t>(H) * 2 * D * 128; }
-
 size_t linear_smem_bytes(int D) {
-  return 1024 + 2 * static_cast<size_t>(D) * 128 + kStages * kABytes + kEpiWarps * kEpiBufs * kStageBytes + 128;
+  return 1024 + static_cast<size_t>(D / 64) * kWBox + kStages * kABytes + kEpiWarps * kEpiBufs * kStageBytes + 128;
 }
 
 bool linear_supported(int H, int F, int D, int num_sms) {
@@ -483,7 +480,7 @@ namespace {
 // {s_z, D s_z, H D s_z, z_stride}; box = 32 rows x 128 bytes of one hop, 128-byte
 // swizzle (the epilogue's staging layout).  False when the driver entry point
 // is unavailable or the encode is rejected (the kernel then uses 16-byte stores).
-bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static bool tried = false;
   if (!tried) {
@@ -494,6 +491,11 @@ bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
         q == cudaDriverEntryPointSuccess)
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+
+bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (encode == nullptr) return false;
   const cuuint64_t z = static_cast<cuuint64_t>(a.z_elem);
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.H),
@@ -506,9 +508,24 @@ bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+// W as a 3-D TMA tensor {column d, row f, hop k} (bf16, byte strides {2 D, 2 F D}),
+// box = 64 columns x 128 rows of one hop, 128-byte swizzle: each box lands as one
+// MN-major SWIZZLE_128B block of the B operand; rows f >= F are filled with zeros.
+bool encode_w_map(const LinearArgs& a, CUtensorMap* m) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (encode == nullptr) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.F), static_cast<cuuint64_t>(a.H)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.D) * 2, static_cast<cuuint64_t>(a.F) * a.D * 2};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kKPad), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.W), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace
 
-cudaError_t launch_gather_linear(const LinearArgs& a_in, cudaStream_t st) {
+cudaError_t launch_gather_linear(const LinearArgs& a_in, bool pdl, cudaStream_t st) {
   if (!linear_supported(a_in.H, a_in.F, a_in.D, a_in.num_sms)) return cudaErrorInvalidValue;
   const size_t smem = linear_smem_bytes(a_in.D);
   static bool attr = false;
@@ -521,14 +538,19 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, cudaStream_t st) {
   LinearArgs a = a_in;
   alignas(64) CUtensorMap zmap{};
   a.z_tma = (a.debug & 128) ? 0 : (encode_z_map(a, &zmap) ? 1 : 0);
-  {
-    const int64_t chunks = static_cast<int64_t>(a.H) * 2 * a.D * 8;
-    const int blocks = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 4 * a.num_sms));
-    k_w_image<<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(a.W), a.H, a.F, a.D, a.w_img);
-  }
-  const int grid = (a.num_sms / a.H) * a.H;
-  k_gather_linear<<<grid, kLinThreads, smem, st>>>(a, zmap);
-  return cudaGetLastError();
+  alignas(64) CUtensorMap wmap{};
+  if (!encode_w_map(a, &wmap)) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
+  cfg.blockDim = dim3(kLinThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  lattr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gather_linear, a, zmap, wmap);
 }
 
 }  // namespace ppl

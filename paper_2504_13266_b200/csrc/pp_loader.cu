@@ -76,8 +76,6 @@ struct pp_loader {
   uint32_t* d_order = nullptr;                  // == d_orders[cur]
   uint32_t* d_pi = nullptr;
   int64_t pi_cap = 0;
-  uint8_t* d_wimg = nullptr;   // fused linear: W_k^T images in the UMMA shared-memory layout
-  size_t wimg_cap = 0;
   SortScratch sort{};
   int sort_bits_max = 0;
   int sort_bits_delta = 0;
@@ -103,7 +101,10 @@ struct pp_loader {
   // Measured on products (profiles/r1j_exp_prefetch.jsonl): full grid 1.002 ms/epoch,
   // 148-296 CTAs 0.972 ms, 64 CTAs 1.11-1.15 ms (the sort then outlasts the epoch).
   int prefetch_ctas = 296;
-  bool last_was_gather = false;  // previous op on the loader stream is a gather of this epoch
+  // previous op on the loader stream (programmatic dependent launch is only used
+  // between consecutive launches of the same kind within one epoch)
+  enum { kLastNone = 0, kLastGather = 1, kLastLinear = 2 };
+  int last_kernel = kLastNone;
 
   ShardView shards[kMaxWorld]{};
   bool linked = false;
@@ -149,7 +150,6 @@ void release(pp_loader* L) {
   cudaFree(L->d_orders[0]);
   cudaFree(L->d_orders[1]);
   cudaFree(L->d_pi);
-  cudaFree(L->d_wimg);
   cudaFree(L->sort.counts);
   cudaFree(L->sort.cursor);
   cudaFree(L->sort.blocksums);
@@ -498,7 +498,7 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
     PPL_CUDA(L, cudaEventRecord(L->ev_out, user));
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_out, 0));
   }
-  L->last_was_gather = false;
+  L->last_kernel = pp_loader::kLastNone;
   return PP_OK;
 }
 
@@ -510,7 +510,7 @@ pp_status pp_set_stream(pp_loader* L, void* stream) {
   if (L->own_stream) cudaStreamDestroy(L->stream);
   L->stream = static_cast<cudaStream_t>(stream);
   L->own_stream = false;
-  L->last_was_gather = false;
+  L->last_kernel = pp_loader::kLastNone;
   return PP_OK;
 }
 
@@ -573,7 +573,7 @@ pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, voi
   }
   L->local = true;
   L->steps = L->desc.drop_last ? L->local_rows / L->B : (L->local_rows + L->B - 1) / L->B;
-  L->last_was_gather = false;
+  L->last_kernel = pp_loader::kLastNone;
   L->permuted = true;
   L->seed = seed;
   L->chunk = chunk;
@@ -624,7 +624,7 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
   }
   L->local = false;
   L->steps = L->steps_global;
-  L->last_was_gather = false;
+  L->last_kernel = pp_loader::kLastNone;
   L->permuted = true;
   L->seed = seed;
   L->chunk = chunk;
@@ -678,7 +678,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
-    L->last_was_gather = false;
+    L->last_kernel = pp_loader::kLastNone;
   }
   if (L->files) {
     // storage tier: each step's rows are read from the hop files, then assembled on the GPU
@@ -697,7 +697,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
       PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
       PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
     }
-    L->last_was_gather = false;
+    L->last_kernel = pp_loader::kLastNone;
     L->cursor += nsteps;
     if (n_done) *n_done = static_cast<int32_t>(nsteps);
     return PP_OK;
@@ -735,8 +735,8 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   // bulk copies when rows come over PCIe (2x the zero-copy LDG rate measured) or NVLink
   const bool remote = L->n_spill > 0 || L->desc.peers == PP_PEERS_IPC;
   if (vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && remote))) path = kPathTma;
-  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_was_gather, L->grid_per_sm, L->stream));
-  L->last_was_gather = !handoff;
+  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_kernel == pp_loader::kLastGather, L->grid_per_sm, L->stream));
+  L->last_kernel = handoff ? pp_loader::kLastNone : pp_loader::kLastGather;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
@@ -801,15 +801,6 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.B = static_cast<int32_t>(L->B);
   a.nsteps = static_cast<int32_t>(nsteps);
   a.W = W;
-  const size_t wimg = linear_w_image_bytes(L->H, D);
-  if (wimg > L->wimg_cap) {
-    cudaFree(L->d_wimg);
-    L->d_wimg = nullptr;
-    L->wimg_cap = 0;
-    PPL_CUDA(L, cudaMalloc(&L->d_wimg, wimg));
-    L->wimg_cap = wimg;
-  }
-  a.w_img = L->d_wimg;
   a.H = L->H;
   a.F = L->F;
   a.D = D;
@@ -827,7 +818,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
     PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, (24 * 14 + 4 * 1024) * 8, L->stream));
     a.ts = dbg_ts;
   }
-  PPL_CUDA(L, launch_gather_linear(a, L->stream));
+  PPL_CUDA(L, launch_gather_linear(a, L->pdl && !handoff && L->last_kernel == pp_loader::kLastLinear, L->stream));
   if (want_ts) {
     static uint64_t h[24 * 14 + 4 * 1024];
     PPL_CUDA(L, cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, L->stream));
@@ -853,7 +844,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
     fprintf(stderr, "cta us (mean/max): entry %.2f/%.2f w_staged %.2f/%.2f prologue_done %.2f/%.2f exit %.2f/%.2f\n",
             sm[0], mx[0], sm[1], mx[1], sm[2], mx[2], sm[3], mx[3]);
   }
-  L->last_was_gather = false;
+  L->last_kernel = handoff ? pp_loader::kLastNone : pp_loader::kLastLinear;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));

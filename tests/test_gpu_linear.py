@@ -114,3 +114,25 @@ def test_fused_linear_rejects_unsupported(pp):
         with pytest.raises(pp.PPError) as ei:
             L.next_batches_linear(1, W, 256, Z, "bf16", 0)  # spilled store
         assert ei.value.status == pp.PP_ERR_INVALID
+
+
+def test_fused_linear_weight_updates_between_calls(pp):
+    # training semantics: W changes after every batch (optimizer step); each call must use the W it is
+    # given (the kernel loads W_k by TMA at every launch, nothing is cached across calls); H = 3 leaves
+    # one SM idle (grid = 147)
+    H, N, F, B, D = 3, 2000, 48, 256, 256
+    X, hs, rs = hop_tensor(66, H, N, F)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(3, 1)
+        order = oracle.epoch_order(3, N, 1)
+        Wd = torch.empty((H, F, D), dtype=torch.bfloat16, device="cuda")
+        Z = torch.empty((1, B, H, D), dtype=torch.float32, device="cuda")
+        for t in range(oracle.num_steps(N, B)):
+            wb = weights(100 + t, H, F, D)
+            Wd.copy_(torch.from_numpy(wb.view(np.int16).copy()).view(torch.bfloat16))  # in place, same pointer
+            rows = L.next_batches_linear(1, Wd, D, Z, "f32", 0)
+            torch.cuda.synchronize()
+            want, _, _ = oracle.batch(X.view(np.uint32), oracle.F32, hs, rs, H, F, order, B, 1, t, 0, oracle.BF16)
+            assert rows == [want.shape[0]]
+            check(Z[0, :rows[0]], "f32", want, wb)
