@@ -110,7 +110,7 @@ struct LinearArgs {
   int32_t num_sms;
   int32_t debug;            // experiment knob (PPLOAD_DEBUG_LINEAR), bits: 1 skip loads, 2 skip Z stores,
                             // 4 skip the drain, 8 skip A-tile stores,
-                            // 64 skip MMAs, 128 no TMA stores (16-byte stores instead)
+                            // 64 skip MMAs, 128 no TMA stores (16-byte stores instead), 256 hop-major Z (timing only)
   int32_t l2_prefetch;      // 1: bulk L2 prefetch of the next tile's rows (PPLOAD_LINEAR_PREFETCH, default 1)
   int32_t z_tma;            // set by launch_gather_linear: Z tensor map encoded, epilogue uses TMA stores
   uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null

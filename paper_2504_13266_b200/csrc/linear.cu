@@ -37,13 +37,20 @@ namespace ppl {
 
 namespace {
 
-constexpr int kEpiWarps = 4;       // one per TMEM lane quadrant (8 measured slower: register spills)
-constexpr int kLinThreads = (12 + kEpiWarps) * 32;  // 0-7 producers, 8 MMA, 9-11 idle, 12.. epilogue
+#ifndef PPL_LIN_EPIWARPS
+#define PPL_LIN_EPIWARPS 4
+#endif
+// Warp roles.  4 epilogue warps: 0-7 producers, 8 MMA, 9-11 idle, 12-15 epilogue.
+// 8 epilogue warps: 0-7 producers, 8-15 epilogue (two per TMEM lane quadrant, each
+// draining half of the columns), 16 MMA -- 17 warps, so ptxas still gets 120 registers.
+constexpr int kEpiWarps = PPL_LIN_EPIWARPS;
+constexpr int kLinThreads = (kEpiWarps == 8 ? 17 : 16) * 32;
 constexpr int kProducerWarps = 8;
 constexpr int kProducerThreads = kProducerWarps * 32;
-constexpr int kMmaWarp = 8;
-constexpr int kEpiWarp0 = 12;      // warps 12..19: TMEM lane quadrant warp % 4, column group (warp-12)/4
-constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kMmaWarp = kEpiWarps == 8 ? 16 : 8;
+constexpr int kEpiWarp0 = kEpiWarps == 8 ? 8 : 12;  // epilogue warp w: lane quadrant w % 4, column group (w - kEpiWarp0) / 4
+constexpr int kEpiGroups = kEpiWarps / 4;
+static_assert(kEpiWarps == 4 || kEpiWarps == 8, "4 or 8 epilogue warps");
 constexpr int kTileM = 128;        // batch rows per tile (UMMA M)
 constexpr int kUmmaN = 256;        // columns per accumulator (UMMA N)
 constexpr int kKPad = 128;         // F zero-padded to two 64-element K blocks
@@ -57,6 +64,10 @@ constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
 constexpr int kStages = PPL_LIN_STAGES;  // A-tile stages
 constexpr int kStageBytes = 32 * 128;  // epilogue staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
 constexpr int kEpiBufs = PPL_LIN_EPIBUFS;  // staging buffers per epilogue warp
+#ifndef PPL_LIN_PFDIST
+#define PPL_LIN_PFDIST 1
+#endif
+constexpr int kPf = PPL_LIN_PFDIST;  // L2 prefetch distance of the producers, in tiles
 constexpr int kWBox = kKPad * 128;  // one TMA box of W_k: 128 K rows x 64 columns (128 B)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   const int k = blockIdx.x % H;                       // this CTA's hop
   const int q = blockIdx.x / H, Q = gridDim.x / H;
   const int nh = D / kUmmaN;                          // accumulators per tile (1 or 2)
+  const int nks = (F + 15) / 16;                      // K steps: columns past F are zero, only whole 16-steps past it are skipped
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -196,7 +208,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     }
     for (int h = 0; h < 2; ++h) {
       bar_init(&t_full[h], 1);
-      bar_init(&t_empty[h], kEpiThreads);
+      // arrivals: every epilogue thread whose column group overlaps accumulator h
+      uint32_t cnt = 0;
+      for (int g = 0; g < kEpiGroups; ++g) {
+        const int lo = g * D / kEpiGroups, hi = (g + 1) * D / kEpiGroups;
+        if (lo < (h + 1) * kUmmaN && hi > h * kUmmaN) cnt += 128;
+      }
+      bar_init(&t_empty[h], cnt > 0 ? cnt : 1);
     }
     bar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -323,18 +341,30 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     };
     uint4 x[16];
     int i = 0;
-    int64_t t = next_tile(q);
-    int64_t t1 = t < total ? next_tile(t + Q) : total;
-    uint32_t idx = fetch_index(t), idx1 = fetch_index(t1);
-    while (t < total) {
-      const int64_t t2 = t1 < total ? next_tile(t1 + Q) : total;
-      load_tile(idx, x);
-      if (a.l2_prefetch) prefetch_rows(idx1);
-      idx = idx1;
-      idx1 = fetch_index(t2);  // in flight together with this tile's data loads
+    // tiles t[0] (loading now), t[1..kPf]; idx[d] = this lane's order[] entry of t[d].
+    // Rows of t[kPf] are prefetched into L2 while t[0] is loaded (kPf tiles ahead).
+    int64_t tq[kPf + 1];
+    uint32_t idx[kPf + 1];
+    tq[0] = next_tile(q);
+#pragma unroll
+    for (int d = 1; d <= kPf; ++d) tq[d] = tq[d - 1] < total ? next_tile(tq[d - 1] + Q) : total;
+#pragma unroll
+    for (int d = 0; d <= kPf; ++d) idx[d] = fetch_index(tq[d]);
+#pragma unroll
+    for (int d = 1; d < kPf; ++d)
+      if (a.l2_prefetch) prefetch_rows(idx[d]);  // the first kPf - 1 tiles ahead
+    while (tq[0] < total) {
+      const int64_t tn = tq[kPf] < total ? next_tile(tq[kPf] + Q) : total;
+      load_tile(idx[0], x);
+      if (a.l2_prefetch) prefetch_rows(idx[kPf]);
+#pragma unroll
+      for (int d = 0; d < kPf; ++d) {
+        idx[d] = idx[d + 1];
+        tq[d] = tq[d + 1];
+      }
+      tq[kPf] = tn;
+      idx[kPf] = fetch_index(tn);  // in flight together with this tile's data loads
       store_tile(i++, x);
-      t = t1;
-      t1 = t2;
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (one lane)
@@ -356,7 +386,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           tc_fence_after();
           if (dbg_lane) dbg_ts(a, i, 4 + 2 * h, 0);
 #pragma unroll
-          for (int ks = 0; ks < ((a.debug & 64) ? 0 : kKPad / 16); ++ks) {
+          for (int ks = 0; ks < ((a.debug & 64) ? 0 : nks); ++ks) {
             const int kb = ks >> 2, j = ks & 3;
             const uint64_t ad = sw128_desc(at + kb * (kTileM * 128)) + 2 * j;  // +32 B per 16-element step
             const uint64_t bd = sw128_mn_desc(w_s + h * (kUmmaN / 64) * kWBox + ks * 2048);  // 16 K rows per step
@@ -381,6 +411,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // A warp whose 32 rows run past the batch (the ragged last step) or a Z
     // without a tensor map writes the staged rows with 16-byte stores instead.
     const int e = warp & 3;                          // TMEM lane quadrant
+    const int grp = (warp - kEpiWarp0) >> 2;         // column group
     uint8_t* sbuf = z_s + (warp - kEpiWarp0) * kEpiBufs * kStageBytes;
     const bool dbg_lane = a.ts != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0;
     const int cols_per_slice = 128 / a.z_elem;
@@ -393,34 +424,44 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       if (rows <= 0) continue;
       const bool tma_rows = a.z_tma && e * 32 + 32 <= rows;
       for (int h = 0; h < nh; ++h) {
+        // this warp's columns of accumulator h: [c_lo, c_hi)
+        const int c_lo = max(grp * D / kEpiGroups, h * kUmmaN) - h * kUmmaN;
+        const int c_hi = min((grp + 1) * D / kEpiGroups, (h + 1) * kUmmaN) - h * kUmmaN;
+        if (c_lo >= c_hi) continue;
         bar_wait(&t_full[h], i & 1);
         tc_fence_after();
         if (dbg_lane) dbg_ts(a, i, 12 + h, 0);
+        // Software-pipelined: the next slice's tcgen05.ld is issued right after this
+        // slice is staged, so its TMEM latency overlaps the fence + TMA store issue.
+        const uint32_t trow = tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN;
+        const int c_end = (a.debug & 4) ? c_lo : c_hi;
+        uint32_t v[64];
+        auto ld_slice = [&](int c0) {
+          PPL_TMEM_LD32(trow + c0, v);
+          if (a.z_elem == 2) PPL_TMEM_LD32(trow + c0 + 32, (v + 32));
+        };
+        if (c_lo < c_end) ld_slice(c_lo);
 #pragma unroll 1
-        for (int c0 = 0; c0 < ((a.debug & 4) ? 0 : kUmmaN); c0 += cols_per_slice, ++slice) {
+        for (int c0 = c_lo; c0 < c_end; c0 += cols_per_slice, ++slice) {
           uint8_t* sb = sbuf + (slice % kEpiBufs) * kStageBytes;
           uint8_t* my = sb + lane * 128;
           // the bulk store issued from this buffer kEpiBufs slices ago must have read it
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
           __syncwarp();
-          for (int c1 = 0; c1 < cols_per_slice; c1 += 32) {  // one tcgen05.ld of 32 columns
-            uint32_t v[32];
-            PPL_TMEM_LD32(tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN + c0 + c1, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int chunk0 = c1 * a.z_elem / 16;  // first 16-byte chunk of this piece in the slice
-            if (a.z_elem == 2) {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (a.z_elem == 2) {
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                *reinterpret_cast<uint4*>(my + (((chunk0 + j) ^ (lane & 7)) << 4)) =
-                    make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                               bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
-            } else {
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                             bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                *reinterpret_cast<uint4*>(my + (((chunk0 + j) ^ (lane & 7)) << 4)) =
-                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
+          if (c0 + cols_per_slice < c_end) ld_slice(c0 + cols_per_slice);
           if (a.debug & 2) continue;
           if (tma_rows) {
             fence_async_smem();  // generic-proxy staging writes -> visible to the bulk-copy engine
@@ -500,8 +541,12 @@ bool encode_z_map(const LinearArgs& a, CUtensorMap* m) {
   const cuuint64_t z = static_cast<cuuint64_t>(a.z_elem);
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.H),
                               static_cast<cuuint64_t>(a.B), static_cast<cuuint64_t>(a.nsteps)};
-  const cuuint64_t strides[3] = {a.D * z, a.H * a.D * z,
-                                 static_cast<cuuint64_t>(a.nsteps > 1 ? a.z_stride : a.B * a.H * a.D * z)};
+  cuuint64_t strides[3] = {a.D * z, a.H * a.D * z,
+                           static_cast<cuuint64_t>(a.nsteps > 1 ? a.z_stride : a.B * a.H * a.D * z)};
+  if (a.debug & 256) {  // experiment only: hop-major Z [step][hop][row][d] (breaks the output contract)
+    strides[0] = a.B * a.D * z;
+    strides[1] = a.D * z;
+  }
   const cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / a.z_elem), 1, 32, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return encode(m, a.z_elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.Z, dims,
