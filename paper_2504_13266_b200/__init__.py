@@ -252,6 +252,10 @@ class Loader:
     def __init__(self, **desc):
         self.h = pp_loader_create(**desc)
         self.info = pp_loader_query(self.h)
+        # per-batch hot path: the C entry point and the out-parameter bound once
+        self._next = lib().pp_next_batch
+        self._rows = ctypes.c_int32()
+        self._rows_ref = ctypes.byref(self._rows)
 
     def close(self):
         if self.h is not None and self.h.value:
@@ -280,7 +284,16 @@ class Loader:
         pp_epoch_prefetch(self.h, seed, chunk)
 
     def next_batch(self, out, out_labels=None, out_nodes=None, consumer_stream=None):
-        return pp_next_batch(self.h, out, out_labels, out_nodes, consumer_stream)
+        """pp_next_batch: rows written, or -1 at the end of the epoch."""
+        rc = self._next(self.h, out.data_ptr() if hasattr(out, "data_ptr") else _ptr(out),
+                        None if out_labels is None else _ptr(out_labels),
+                        None if out_nodes is None else _ptr(out_nodes), self._rows_ref,
+                        None if consumer_stream is None else _stream(consumer_stream))
+        if rc == PP_OK:
+            return self._rows.value
+        if rc == PP_END_OF_EPOCH:
+            return -1
+        _check(rc, "pp_next_batch")
 
     def next_batches(self, n, out, out_stride_bytes, out_labels=None, out_nodes=None, consumer_stream=None):
         return pp_next_batches(self.h, n, out, out_stride_bytes, out_labels, out_nodes, consumer_stream)

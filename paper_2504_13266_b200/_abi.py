@@ -88,6 +88,8 @@ _lib = None
 def lib():
     """Load libppload.so.  Raises if it has not been built (no fallback)."""
     global _lib
+    if _lib is not None:  # fast path: no lock once loaded
+        return _lib
     with _lock:
         if _lib is None:
             if not os.path.exists(LIB_PATH):

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -290,17 +291,28 @@ pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64
   if (e != cudaSuccess) return fail(PP_ERR_CUDA, "hop 0 copy: %s", cudaGetErrorString(e));
   if (K == 0) return PP_OK;
   double* val = nullptr;
-  {  // keep the stream-ordered pool's memory between calls (the default threshold unmaps it at every sync)
-    static bool pool_set = false;
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (!pool_set && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  // stream-ordered scratch from a library-private pool (per device) that keeps its memory
+  // between calls; the device's default pool and its release threshold are left alone
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(PP_ERR_CUDA, "cudaGetDevice failed");
+  {
+    static std::mutex pools_mu;
+    std::lock_guard<std::mutex> lk(pools_mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t pool = nullptr;
+      if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return fail(PP_ERR_CUDA, "cudaMemPoolCreate failed");
       uint64_t keep = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      pool_set = true;
+      pools[dev] = pool;
     }
   }
-  if (cudaMallocAsync(reinterpret_cast<void**>(&val), static_cast<size_t>(nnz) * sizeof(double), st) != cudaSuccess)
+  if (cudaMallocFromPoolAsync(reinterpret_cast<void**>(&val), static_cast<size_t>(nnz) * sizeof(double), pools[dev],
+                              st) != cudaSuccess)
     return fail(PP_ERR_OOM, "operator values (%lld nonzeros)", (long long)nnz);
   e = launch_operator_values(n, row_ptr, col_idx, val, st);
   for (int32_t k = 1; k <= K && e == cudaSuccess; ++k)
