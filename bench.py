@@ -311,13 +311,18 @@ def run_ours(args):
                                             f"{ring.numel() * 2 / 1e9:.2f} GB ring of {nslots} slots"),
         "roofline": roofline, "gpu_launches": (perm_kernels + m["launches"]) * args.steps, "clocks": m["clocks"],
         "batches_per_launch": k, "prefetch_next_epoch_order": bool(args.prefetch),
+        # SURVEY.md §8(d) timing protocol: (a) gather-only nodes/s (span of the epoch's gathers),
+        # (b) whole epochs incl. the permutation (= value), (c) per-call latency (per_batch_call)
+        "gather_only": {"value": N * args.steps / (m["gather_ms"] / 1e3), "unit": UNIT,
+                        "ms_per_epoch": m["gather_ms"] / args.steps},
     }
     if k != 1 and not args.skip_k1:
         m1 = timed(1, max(3, args.steps // 2))
         result["per_batch_call"] = {
             "value": N * max(3, args.steps // 2) / (m1["total_ms"] / 1e3), "unit": UNIT,
             "ms_per_step": m1["total_ms"] / max(3, args.steps // 2), "achieved_GBs": m1["achieved"],
-            "note": "one pp_next_batch call (one launch) per batch from Python; host-bound (~5.6 us per ctypes call)"}
+            "per_call_us": m1["total_ms"] * 1e3 / (max(3, args.steps // 2) * steps),
+            "note": "one pp_next_batch call (one launch) per batch from Python (Loader.next_batch fast path)"}
     del ring
     torch.cuda.synchronize()
     if dist:
