@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 3
+#define PP_ABI_VERSION 4
 
 /* Bytes of one rank's exported store handle (pp_export_store). */
 #define PP_IPC_HANDLE_BYTES 128
@@ -132,13 +132,22 @@ typedef struct {
   pp_peers peers;           /* PP_PEERS_NONE iff W == 1 (file loaders: always
                                PP_PEERS_NONE, any W) */
   int32_t device;           /* CUDA device ordinal */
+  int32_t store_set_only;   /* 1: the store holds only the node_set rows ("the input
+                               data size after preprocessing is proportional to the
+                               number of labeled nodes"): record i is
+                               node node_set[i]; sharding (W > 1) is over node-set
+                               positions (owner i mod W).  Needs node_set and an
+                               in-memory source; batches are identical to the full
+                               store's.  Not with pp_propagate_store (which needs
+                               every node).  0: every node has a record. */
 } pp_loader_desc;
 
 /* Read-only facts about a loader (pp_loader_query). */
 typedef struct {
   int64_t num_positions;    /* N: |node_set| or N_total */
   int64_t num_nodes_total;  /* N_total */
-  int64_t local_rows;       /* rows owned by this rank */
+  int64_t local_rows;       /* records owned by this rank (node ids, or node-set positions
+                               with store_set_only) */
   int64_t rows_hbm;         /* of which in HBM */
   int64_t rows_spill;       /* of which in pinned host memory (UVA) */
   int64_t record_bytes_in;  /* H*F*s_in: bytes of one node record in the store */

@@ -56,6 +56,7 @@ class pp_loader_desc(ctypes.Structure):
         ("rank", ctypes.c_int32),
         ("peers", ctypes.c_int),
         ("device", ctypes.c_int32),
+        ("store_set_only", ctypes.c_int32),
     ]
 
 

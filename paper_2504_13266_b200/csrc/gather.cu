@@ -97,8 +97,9 @@ __device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, 
     else
       s_src[threadIdx.x] = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
     const int64_t oj = step * a.B + j0 + threadIdx.x;
-    if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
-    if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
+    const uint64_t id = a.out_ids != nullptr ? static_cast<uint64_t>(a.out_ids[v]) : v;
+    if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[id];
+    if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(id);
   }
 }
 
@@ -327,8 +328,9 @@ __global__ void __launch_bounds__(kGatherThreads, 2)
     if (j < rows) {
       bulk_g2s(stage + static_cast<int64_t>(j) * rec_in, src, bytes, &full[s]);
       const int64_t oj = step * a.B + j0 + j;
-      if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[v];
-      if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(v);
+      const uint64_t id = a.out_ids != nullptr ? static_cast<uint64_t>(a.out_ids[v]) : v;
+      if (a.out_labels != nullptr) a.out_labels[oj] = a.labels[id];
+      if (a.out_nodes != nullptr) a.out_nodes[oj] = static_cast<int64_t>(id);
     }
   };
   if (warp == 0)
@@ -500,7 +502,8 @@ cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_
 
 // ---- K10: synthetic fill (SURVEY.md §8(d) generators G / G16) ----------------
 __global__ void k_fill_synthetic(uint8_t* __restrict__ base, int64_t row0, int64_t nrows, int64_t rec_stride,
-                                 int32_t H, int32_t F, int32_t dtype, uint64_t seed, int32_t W, int32_t rank) {
+                                 int32_t H, int32_t F, int32_t dtype, uint64_t seed, int32_t W, int32_t rank,
+                                 const int64_t* __restrict__ ids) {
   const int32_t F4 = (F + 3) / 4;
   const int64_t total = nrows * H * F4;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -509,7 +512,8 @@ __global__ void k_fill_synthetic(uint8_t* __restrict__ base, int64_t row0, int64
     const int32_t rem = static_cast<int32_t>(t - row * H * F4);
     const int32_t k = rem / F4;
     const int32_t f4 = rem - k * F4;
-    const uint64_t v = static_cast<uint64_t>(row0 + row) * W + rank;  // global node id
+    const uint64_t x = static_cast<uint64_t>(row0 + row) * W + rank;  // row space index of this record
+    const uint64_t v = ids != nullptr ? static_cast<uint64_t>(ids[x]) : x;  // global node id
     const uint4 w4 = synth_block(seed, v, static_cast<uint32_t>(k), static_cast<uint32_t>(f4));
     const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
     uint8_t* rec = base + row * rec_stride;
@@ -529,9 +533,39 @@ __global__ void k_fill_synthetic(uint8_t* __restrict__ base, int64_t row0, int64
 
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
                                   int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,
-                                  cudaStream_t st) {
+                                  const int64_t* ids, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
-  k_fill_synthetic<<<148 * 16, 256, 0, st>>>(base, row0, nrows, rec_stride, H, F, dtype, data_seed, W, rank);
+  k_fill_synthetic<<<148 * 16, 256, 0, st>>>(base, row0, nrows, rec_stride, H, F, dtype, data_seed, W, rank, ids);
+  return cudaGetLastError();
+}
+
+// Compact store from a device source: record r = the H hop vectors of node ids[r*W + rank]
+// (element strides hop_stride / row_stride of the source), elem = 2 or 4 bytes.
+__global__ void k_pack_rows(const uint8_t* __restrict__ src, int64_t hop_stride, int64_t row_stride, int32_t elem,
+                            int32_t H, int32_t F, const int64_t* __restrict__ ids, int64_t nrows, int32_t W,
+                            int32_t rank, uint8_t* __restrict__ dst, int64_t rec_stride) {
+  const int64_t total = nrows * H * F;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / (static_cast<int64_t>(H) * F);
+    const int32_t kf = static_cast<int32_t>(t - r * H * F);
+    const int32_t k = kf / F, f = kf - k * F;
+    const int64_t v = ids[r * W + rank];
+    const int64_t e = k * hop_stride + v * row_stride + f;
+    uint8_t* d = dst + r * rec_stride + static_cast<int64_t>(kf) * elem;
+    if (elem == 4)
+      *reinterpret_cast<uint32_t*>(d) = reinterpret_cast<const uint32_t*>(src)[e];
+    else
+      *reinterpret_cast<uint16_t*>(d) = reinterpret_cast<const uint16_t*>(src)[e];
+  }
+}
+
+cudaError_t launch_pack_rows(const void* src, int64_t hop_stride, int64_t row_stride, int32_t elem, int32_t H,
+                             int32_t F, const int64_t* ids, int64_t nrows, int32_t W, int32_t rank, uint8_t* dst,
+                             int64_t rec_stride, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  k_pack_rows<<<148 * 16, 256, 0, st>>>(static_cast<const uint8_t*>(src), hop_stride, row_stride, elem, H, F, ids,
+                                        nrows, W, rank, dst, rec_stride);
   return cudaGetLastError();
 }
 

@@ -63,7 +63,9 @@ cudaError_t launch_local_to_global(uint32_t* order, int64_t n, int32_t W, int32_
 // ---- batch assembly (gather.cu) ----------------------------------------------
 struct GatherArgs {
   const uint32_t* order;    // positions -> index into node set (or node id)
-  const int64_t* node_set;  // may be null
+  const int64_t* node_set;  // row resolution: store row space index x -> node_set[x]; null: x itself
+  const int64_t* out_ids;   // compact store: output node ids / labels via out_ids[x] (rows are node-set
+                            // positions); null: the resolved row id is the node id
   const int32_t* labels;    // may be null
   int64_t N;                // positions in an epoch
   int64_t first_pos;        // first position of this rank in the first step
@@ -150,9 +152,14 @@ cudaError_t launch_cast_records(const uint8_t* src, int64_t rows, int64_t rec_st
                                 uint8_t* dst, int64_t xrec_stride, cudaStream_t st);
 
 // ---- synthetic fill (gather.cu) ---------------------------------------------
+// ids (compact store): record x holds node ids[x] (x = row0 + row, times W plus rank); null: node x.
 cudaError_t launch_fill_synthetic(uint8_t* base, int64_t row0, int64_t nrows, int64_t rec_stride, int32_t H,
                                   int32_t F, int32_t dtype, uint64_t data_seed, int32_t W, int32_t rank,
-                                  cudaStream_t st);
+                                  const int64_t* ids, cudaStream_t st);
+// Compact store upload from a device source (see k_pack_rows).
+cudaError_t launch_pack_rows(const void* src, int64_t hop_stride, int64_t row_stride, int32_t elem, int32_t H,
+                             int32_t F, const int64_t* ids, int64_t nrows, int32_t W, int32_t rank, uint8_t* dst,
+                             int64_t rec_stride, cudaStream_t st);
 
 // ---- storage tier (storage.cu) ----------------------------------------------
 struct FileTier;

@@ -115,6 +115,8 @@ struct pp_loader {
   FileTier* files = nullptr;
   std::vector<uint32_t> h_order;      // host copy of the current epoch's order
   std::vector<int64_t> h_node_set;    // host copy of the node set (empty: identity)
+  // compact store (desc.store_set_only): records are node-set positions, not node ids
+  bool compact = false;
   uint64_t epoch_id = 0;              // bumped by every permute / seek (invalidates staged steps)
 
   bool permuted = false, poisoned = false;
@@ -187,6 +189,47 @@ cudaError_t copy_in(const pp_loader* L, const pp_hop_desc& h, int64_t row0, int6
   return cudaSuccess;
 }
 
+// Compact store (store_set_only): record lr of rank r holds node S[lr*W + r] of the
+// node set S.  Device sources are packed by a kernel; host sources row by row on the
+// host, into the pinned spill directly or through a pinned staging buffer.
+cudaError_t copy_in_compact(const pp_loader* L, const pp_hop_desc& h, const int64_t* S_host, int64_t row0, int64_t n,
+                            uint8_t* dst, bool dst_is_host) {
+  const int s = elem_bytes(h.dtype);
+  if (n <= 0) return cudaSuccess;
+  if (h.where == PP_MEM_DEVICE) {
+    cudaError_t e = launch_pack_rows(h.data, h.hop_stride, h.row_stride, s, L->H, L->F, L->d_node_set + row0 * L->W, n,
+                                     L->W, L->rank, dst_is_host ? L->d_spill + (dst - L->h_spill) : dst,
+                                     L->rec_stride, nullptr);
+    return e == cudaSuccess ? cudaDeviceSynchronize() : e;
+  }
+  const uint8_t* src = static_cast<const uint8_t*>(h.data);
+  const size_t rb = static_cast<size_t>(L->F) * s;
+  auto pack = [&](uint8_t* out, int64_t r0, int64_t m) {
+    for (int64_t r = 0; r < m; ++r) {
+      const int64_t v = S_host[(row0 + r0 + r) * L->W + L->rank];
+      for (int32_t k = 0; k < L->H; ++k)
+        memcpy(out + r * L->rec_stride + static_cast<size_t>(k) * rb,
+               src + (static_cast<int64_t>(k) * h.hop_stride + v * h.row_stride) * s, rb);
+    }
+  };
+  if (dst_is_host) {
+    pack(dst, 0, n);
+    return cudaSuccess;
+  }
+  const int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / L->rec_stride);
+  uint8_t* stage = nullptr;
+  if (cudaHostAlloc(&stage, static_cast<size_t>(std::min(chunk, n) * L->rec_stride), cudaHostAllocDefault) != cudaSuccess)
+    return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaSuccess;
+  for (int64_t a = 0; a < n && e == cudaSuccess; a += chunk) {
+    const int64_t m = std::min(chunk, n - a);
+    pack(stage, a, m);
+    e = cudaMemcpy(dst + a * L->rec_stride, stage, static_cast<size_t>(m * L->rec_stride), cudaMemcpyHostToDevice);
+  }
+  cudaFreeHost(stage);
+  return e;
+}
+
 // The prefetched permutation runs at the lowest stream priority so the block
 // scheduler serves the current epoch's gathers first.
 int prefetch_priority() {
@@ -209,6 +252,8 @@ pp_status validate(const pp_loader_desc* d) {
   const bool files = h.where == PP_MEM_FILES;
   if (files && !h.data) return fail(PP_ERR_INVALID, "PP_MEM_FILES needs the array of H hop file paths");
   if (files && d->peers != PP_PEERS_NONE) return fail(PP_ERR_INVALID, "file loaders take peers = PP_PEERS_NONE");
+  if (d->store_set_only && (!d->node_set || files))
+    return fail(PP_ERR_INVALID, "store_set_only needs a node_set and an in-memory source");
   const bool cast = h.dtype == PP_F32 && (d->out_dtype == PP_BF16 || d->out_dtype == PP_F16);
   if (!cast && h.dtype != d->out_dtype)
     return fail(PP_ERR_INVALID, "unsupported dtype pair (store %d -> out %d)", h.dtype, d->out_dtype);
@@ -357,7 +402,10 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   const int64_t per_step = L->B * L->W;
   L->steps = desc->drop_last ? L->N / per_step : (L->N + per_step - 1) / per_step;
   L->steps_global = L->steps;
-  L->local_rows = (L->N_total - L->rank + L->W - 1) / L->W;
+  L->compact = desc->store_set_only != 0;
+  // row space of the store: node ids 0..N_total-1, or node-set positions 0..N-1 (compact)
+  const int64_t R = L->compact ? L->N : L->N_total;
+  L->local_rows = (R - L->rank + L->W - 1) / L->W;
   L->rec_in = static_cast<int64_t>(L->HF) * elem_bytes(L->in_dtype);
   L->rec_stride = (L->rec_in + 15) / 16 * 16;
   L->rec_out = static_cast<int64_t>(L->HF) * elem_bytes(L->out_dtype);
@@ -378,6 +426,11 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (desc->node_set) L->h_node_set.assign(desc->node_set, desc->node_set + L->N);
   }
 
+  if (desc->node_set) {  // before the store upload (the compact store is packed through it)
+    if (cudaMalloc(&L->d_node_set, L->N * 8) != cudaSuccess) return bail(fail(PP_ERR_OOM, "node_set allocation"));
+    if (cudaMemcpy(L->d_node_set, desc->node_set, L->N * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(PP_ERR_CUDA, "node_set upload"));
+  }
   // ---- placement: HBM budget, remainder spills to pinned mapped host memory
   const int64_t scratch = L->N * 4 * 3 + (int64_t(1) << 26) + (L->has_labels ? L->N_total * 4 : 0);
   int64_t budget = desc->hbm_budget_bytes;
@@ -403,17 +456,17 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->d_spill), L->h_spill, 0) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "cudaHostGetDevicePointer failed"));
   }
-  if (desc->hops.data && !files) {
+  if (desc->hops.data && !files && L->compact) {
+    cudaError_t e = copy_in_compact(L, desc->hops, desc->node_set, 0, L->n_hbm, L->d_store, false);
+    if (e == cudaSuccess && L->n_spill > 0)
+      e = copy_in_compact(L, desc->hops, desc->node_set, L->n_hbm, L->n_spill, L->h_spill, true);
+    if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
+  } else if (desc->hops.data && !files) {
     cudaError_t e = copy_in(L, desc->hops, 0, L->n_hbm, L->d_store);
     if (e == cudaSuccess && L->n_spill > 0) e = copy_in(L, desc->hops, L->n_hbm, L->n_spill, L->h_spill);
     if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
   }
-  // ---- node set, labels, order, sort scratch
-  if (desc->node_set) {
-    if (cudaMalloc(&L->d_node_set, L->N * 8) != cudaSuccess) return bail(fail(PP_ERR_OOM, "node_set allocation"));
-    if (cudaMemcpy(L->d_node_set, desc->node_set, L->N * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(PP_ERR_CUDA, "node_set upload"));
-  }
+  // ---- labels, order, sort scratch
   if (desc->labels) {
     L->has_labels = true;
     if (cudaMalloc(&L->d_labels, L->N_total * 4) != cudaSuccess) return bail(fail(PP_ERR_OOM, "labels allocation"));
@@ -481,7 +534,8 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!row_ptr || !col_idx || !deg) return fail(PP_ERR_INVALID, "NULL CSR / degree pointer");
-  if (L->in_dtype != PP_F32 || L->files) return fail(PP_ERR_INVALID, "pp_propagate_store needs an fp32 store");
+  if (L->in_dtype != PP_F32 || L->files || L->compact)
+    return fail(PP_ERR_INVALID, "pp_propagate_store needs an fp32 store of every node (not compact)");
   if (k < 1 || k >= L->H) return fail(PP_ERR_INVALID, "hop slot k = %d must be in [1, H-1 = %d]", k, L->H - 1);
   if (L->F > 256) return fail(PP_ERR_INVALID, "F = %d > 256", L->F);
   if (!L->linked) return fail(PP_ERR_STATE, "sharded loader not linked to its peers yet");
@@ -716,7 +770,8 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   }
   GatherArgs a{};
   a.order = L->d_order;
-  a.node_set = L->d_node_set;
+  a.node_set = L->compact ? nullptr : L->d_node_set;  // compact: rows are node-set positions
+  a.out_ids = L->compact ? L->d_node_set : nullptr;
   a.labels = L->d_labels;
   // global epoch: step t of rank r = positions [tWB + rB, ...) of the shared order;
   // local epoch: step t = positions [tB, ...) of this rank's own order
@@ -804,7 +859,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   }
   LinearArgs a{};
   a.order = L->d_order;
-  a.node_set = L->d_node_set;
+  a.node_set = L->compact ? nullptr : L->d_node_set;
   a.store = L->d_store;
   a.rec_stride = L->rec_stride;
   a.N = L->N;
@@ -905,10 +960,11 @@ pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed) {
   if (L->in_dtype == PP_BF16) return fail(PP_ERR_INVALID, "no synthetic generator for bf16 stores");
   if (L->files) return fail(PP_ERR_INVALID, "file loaders have no store to fill");
   DevGuard g(L->dev);
+  const int64_t* ids = L->compact ? L->d_node_set : nullptr;
   PPL_CUDA(L, launch_fill_synthetic(L->d_store, 0, L->n_hbm, L->rec_stride, L->H, L->F, L->in_dtype, data_seed, L->W,
-                                    L->rank, L->stream));
+                                    L->rank, ids, L->stream));
   PPL_CUDA(L, launch_fill_synthetic(L->d_spill, L->n_hbm, L->n_spill, L->rec_stride, L->H, L->F, L->in_dtype,
-                                    data_seed, L->W, L->rank, L->stream));
+                                    data_seed, L->W, L->rank, ids, L->stream));
   PPL_CUDA(L, cudaStreamSynchronize(L->stream));
   PPL_CUDA(L, refresh_exchange_copy(L));
   return PP_OK;
@@ -982,7 +1038,8 @@ pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
       PPL_CUDA(L, cudaIpcOpenMemHandle(&x, h, cudaIpcMemLazyEnablePeerAccess));
       L->ipc_opened.push_back(x);
     }
-    const int64_t rows_o = (L->N_total - o + L->W - 1) / L->W;  // whole shard in HBM (checked at create)
+    const int64_t R = L->compact ? L->N : L->N_total;
+    const int64_t rows_o = (R - o + L->W - 1) / L->W;  // whole shard in HBM (checked at create)
     L->shards[o] = ShardView{static_cast<const uint8_t*>(p), nullptr, rows_o, static_cast<const uint8_t*>(x)};
   }
   L->linked = true;
@@ -998,7 +1055,8 @@ pp_status pp_link_loopback(pp_loader* const* Ls, int32_t W) {
       return fail(PP_ERR_INVALID, "loader %d: not a loopback rank %d of %d", r, r, W);
     if (L->dev != Ls[0]->dev || L->H != Ls[0]->H || L->F != Ls[0]->F || L->in_dtype != Ls[0]->in_dtype ||
         L->N_total != Ls[0]->N_total || L->rec_stride != Ls[0]->rec_stride ||
-        L->out_dtype != Ls[0]->out_dtype || L->xrec_stride != Ls[0]->xrec_stride)
+        L->out_dtype != Ls[0]->out_dtype || L->xrec_stride != Ls[0]->xrec_stride || L->compact != Ls[0]->compact ||
+        L->N != Ls[0]->N)
       return fail(PP_ERR_INVALID, "loader %d: store shape differs from rank 0", r);
   }
   for (int r = 0; r < W; ++r) {

@@ -52,7 +52,7 @@ def _header_define(name):
 
 
 def test_abi_version_and_footprint(pp):
-    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 3
+    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 4
     assert pp.IPC_HANDLE_BYTES == _header_define("PP_IPC_HANDLE_BYTES")
     # input expansion K(R+1)x: 400 GB at R = 3, K = 1 -> 1.6 TB
     n = 100_000_000
@@ -94,3 +94,37 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).replace("oracle/", ""), f
+
+
+def test_struct_layouts_match_header(tmp_path):
+    # the ctypes mirrors must have the header's exact layout (sizes and field offsets), checked by
+    # compiling a probe against include/pp_loader.h with the host C compiler
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2504_13266_b200 import _abi
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no host C compiler")
+    structs = {"pp_hop_desc": _abi.pp_hop_desc, "pp_loader_desc": _abi.pp_loader_desc,
+               "pp_loader_info": _abi.pp_loader_info}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pp_loader.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for field, _ in cls._fields_:
+            lines.append(f'  printf("{name} {field} %zu\\n", offsetof({name}, {field}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "probe"
+    subprocess.check_call([cc, "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = {}
+    for line in subprocess.check_output([str(exe)], text=True).splitlines():
+        name, what, val = line.split()
+        got[(name, what)] = int(val)
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for field, _ in cls._fields_:
+            assert got[(name, field)] == getattr(cls, field).offset, (name, field)
