@@ -4,6 +4,8 @@
   papers100M-1r : configs[2] row shape (F = 128, K = 3, fp32 -> bf16, B = 8192, c = 8192) on one
                   rank's store at W = 2 (55.5 M rows, 114 GB, HBM-resident) -- the full 227 GB
                   store does not fit one GPU
+  papers100M-labelled : the paper's papers100M setup: a compact store of the
+                  1.55 M labelled nodes of 111 M (3.2 GB), RR and c = 8192
   mag240m-1r    : configs[4] row shape (F = 768, K = 3, fp16 -> fp16 copy, B = 8192, RR) on a
                   25 M-row store (154 GB, HBM-resident)
   igb-large-scaled : configs[3] row shape (F = 1024, K = 2, fp32 -> bf16, B = 4096, RR) on a
@@ -27,11 +29,15 @@ PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEAS
 
 
 def measure(name, N, H, F, B, chunk, dtype, out_dtype, budget=0, epochs=5, k=8, max_ring_gb=8.0, bound="hbm",
-            pcie_peak=None):
+            pcie_peak=None, node_set=None):
     s_in = 4 if dtype == pp.PP_F32 else 2
     s_out = 4 if out_dtype == pp.PP_F32 else 2
+    extra = dict(node_set=node_set, store_set_only=True) if node_set is not None else {}
     L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=dtype, batch_size=B, out_dtype=out_dtype,
-                  hbm_budget_bytes=budget)
+                  hbm_budget_bytes=budget, **extra)
+    N_total = N
+    if node_set is not None:
+        N = node_set.shape[0]  # positions per epoch
     L.fill_synthetic(2504)
     st = torch.cuda.Stream()
     L.set_stream(st)
@@ -65,7 +71,7 @@ def measure(name, N, H, F, B, chunk, dtype, out_dtype, budget=0, epochs=5, k=8, 
     ms = a.elapsed_time(b) / epochs
     per_node = H * F * (s_in + s_out) + 4
     hbm_gbs = N * per_node / ms / 1e6
-    out = dict(config=name, N=N, H=H, F=F, B=B, chunk=chunk, ms_per_epoch=ms, nodes_per_s=N / ms * 1e3,
+    out = dict(config=name, N=N, N_total=N_total, H=H, F=F, B=B, chunk=chunk, ms_per_epoch=ms, nodes_per_s=N / ms * 1e3,
                algorithmic_bytes_per_node=per_node, achieved_GBs=hbm_gbs, rows_hbm=info["rows_hbm"],
                rows_spill=info["rows_spill"], ring_slots=nslots)
     if bound == "hbm":
@@ -95,11 +101,20 @@ def dma_peak():
     return gbs
 
 
-which = sys.argv[1:] or ["products-CR", "papers100M-1r", "mag240m-1r", "igb-large-scaled"]
+which = sys.argv[1:] or ["products-CR", "papers100M-1r", "papers100M-labelled", "mag240m-1r", "igb-large-scaled"]
 if "products-CR" in which:
     measure("products-CR", 2_449_029, 4, 100, 8192, 8192, pp.PP_F32, pp.PP_BF16, epochs=10)
 if "papers100M-1r" in which:
     measure("papers100M-1r", 55_529_978, 4, 128, 8192, 8192, pp.PP_F32, pp.PP_BF16)
+if "papers100M-labelled" in which:
+    # the paper's own papers100M setup: only the labelled nodes' hop features are
+    # kept (0.8 GB per hop, ~1.55 M of 111 M nodes; compact store), so it fits one GPU
+    import numpy as np
+
+    S = np.random.default_rng(2504).choice(111_059_956, size=1_546_782, replace=False).astype(np.int64)
+    for c in (1, 8192):
+        measure(f"papers100M-labelled-c{c}", 111_059_956, 4, 128, 8192, c, pp.PP_F32, pp.PP_BF16, epochs=10,
+                node_set=S)
 if "mag240m-1r" in which:
     measure("mag240m-1r", 25_000_000, 4, 768, 8192, 1, pp.PP_F16, pp.PP_F16, epochs=3)
 if "igb-large-scaled" in which:
