@@ -189,3 +189,4 @@ def test_invalid_file_loaders(pp, tmp_path):
             call()
         assert ei.value.status == pp.PP_ERR_INVALID
     L.close()
+
