@@ -212,8 +212,11 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk);
  * last step; may be 0 on high ranks of the last step for W > 1).
  * Stream semantics: `out` is written after all work enqueued on
  * consumer_stream before this call, and is valid for work enqueued on
- * consumer_stream after it.  Alternating two buffers therefore overlaps the
- * assembly of batch t+1 with the consumer's work on batch t (double buffer).
+ * consumer_stream after it.  This orders the batch simply but cannot overlap
+ * it with the consumer: the call both waits for and is waited on by the same
+ * point of consumer_stream.  For the paper's double buffer (PAPER.md:262-263:
+ * batch t+1 assembled while the consumer works on batch t) use
+ * pp_next_batches_ev with per-buffer events.
  * When consumer_stream is the loader stream (pp_set_stream), consecutive
  * batches of one epoch may execute concurrently (programmatic dependent
  * launch): give each call its own buffer, or put the consumer's kernels
@@ -232,6 +235,21 @@ pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* o
 pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes,
                           int32_t* out_labels, int64_t* out_nodes, int32_t* rows,
                           int32_t* n_done, void* consumer_stream);
+
+/* pp_next_batches with explicit events instead of a consumer stream -- the
+ * double buffer.  wait_event (cudaEvent_t or NULL): the
+ * assembly waits for it before writing `out` (record it on the consumer's stream
+ * after the consumer's last use of these slots).  ready_event (cudaEvent_t or
+ * NULL): recorded on the loader stream once the slots are written; the consumer
+ * waits for it before reading them.  With two buffers A/B the loop is
+ *   next(A, wait=NULL, ready=rA)
+ *   for t: next(other, wait=free[other], ready=r[other]);  consumer: wait r[cur],
+ *          step(cur), record free[cur]
+ * so batch t+1 is assembled while step t runs.  Other semantics (cursor, rows,
+ * n_done, errors) as pp_next_batches. */
+pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes, int32_t* out_labels,
+                             int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* wait_event,
+                             void* ready_event);
 
 /* Consumer fusion: assemble the next n steps AND apply
  * SIGN's per-hop linear layer ("learns R+1 weight matrices for each hop",
@@ -310,6 +328,14 @@ pp_status pp_seek(pp_loader* L, int64_t step);
 /* Use `stream` as the loader stream (default: a library-created non-blocking
  * stream).  When consumer_stream == loader stream, no events are recorded. */
 pp_status pp_set_stream(pp_loader* L, void* stream);
+
+/* Cap the batch-assembly grid at max_ctas CTAs (0: the full persistent grid,
+ * default).  A loader whose batches overlap a consumer on the same GPU (the
+ * double buffer, pp_next_batches_ev) otherwise takes every SM while it runs;
+ * a PCIe-bound (host-resident) gather needs only a few CTAs to keep the link
+ * busy.  Applies to later pp_next_batch / pp_next_batches(_ev) calls.
+ * Errors: PP_ERR_INVALID (max_ctas < 0). */
+pp_status pp_set_grid_limit(pp_loader* L, int32_t max_ctas);
 
 pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info);
 

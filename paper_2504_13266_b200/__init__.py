@@ -27,7 +27,8 @@ __all__ = [
     "pp_seek", "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
     "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
-    "pp_epoch_permute_local", "pp_propagate_store",
+    "pp_epoch_permute_local", "pp_propagate_store", "pp_next_batches_ev",
+    "pp_set_grid_limit",
 ]
 
 
@@ -168,6 +169,27 @@ def pp_next_batches(h, n, out, out_stride_bytes, out_labels=None, out_nodes=None
     return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
 
 
+def _event(e):
+    if e is None:
+        return None
+    if isinstance(e, int):
+        return e
+    return e.cuda_event  # torch.cuda.Event
+
+
+def pp_next_batches_ev(h, n, out, out_stride_bytes, out_labels=None, out_nodes=None, wait_event=None,
+                       ready_event=None):
+    """Event-ordered pp_next_batches (double buffer): waits for ``wait_event`` before writing,
+    records ``ready_event`` when the slots are written (torch.cuda.Event or raw cudaEvent_t).
+    Returns the list of rows per assembled step ([] at the end of the epoch)."""
+    rows = (ctypes.c_int32 * n)()
+    done = ctypes.c_int32()
+    rc = lib().pp_next_batches_ev(h, n, _ptr(out), out_stride_bytes, _ptr(out_labels), _ptr(out_nodes), rows,
+                                  ctypes.byref(done), _event(wait_event), _event(ready_event))
+    _check(rc, "pp_next_batches_ev", ok=(PP_OK, PP_END_OF_EPOCH))
+    return [] if rc == PP_END_OF_EPOCH else list(rows[: done.value])
+
+
 def pp_next_batches_linear(h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream=None):
     """Fused batch assembly + per-hop linear (tensor cores).  Returns rows per step ([] at epoch end)."""
     rows = (ctypes.c_int32 * n)()
@@ -191,6 +213,10 @@ def pp_propagate_store(h, k: int, row_ptr, col_idx, deg, stream=None) -> None:
     local CSR (global columns), device int32 global degrees d~."""
     _check(lib().pp_propagate_store(h, k, _ptr(row_ptr), _ptr(col_idx), _ptr(deg), _stream(stream)),
            "pp_propagate_store")
+
+
+def pp_set_grid_limit(h, max_ctas: int) -> None:
+    _check(lib().pp_set_grid_limit(h, max_ctas), "pp_set_grid_limit")
 
 
 def pp_seek(h, step: int) -> None:
@@ -300,11 +326,18 @@ class Loader:
     def next_batches(self, n, out, out_stride_bytes, out_labels=None, out_nodes=None, consumer_stream=None):
         return pp_next_batches(self.h, n, out, out_stride_bytes, out_labels, out_nodes, consumer_stream)
 
+    def next_batches_ev(self, n, out, out_stride_bytes, out_labels=None, out_nodes=None, wait_event=None,
+                        ready_event=None):
+        return pp_next_batches_ev(self.h, n, out, out_stride_bytes, out_labels, out_nodes, wait_event, ready_event)
+
     def next_batches_linear(self, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream=None):
         return pp_next_batches_linear(self.h, n, W, D, Z, z_dtype, z_stride_bytes, consumer_stream)
 
     def propagate_store(self, k, row_ptr, col_idx, deg, stream=None):
         pp_propagate_store(self.h, k, row_ptr, col_idx, deg, stream)
+
+    def set_grid_limit(self, max_ctas):
+        pp_set_grid_limit(self.h, max_ctas)
 
     def seek(self, step):
         pp_seek(self.h, step)

@@ -19,7 +19,8 @@ EXPORTS = [
     "pp_set_stream", "pp_loader_query", "pp_last_error", "pp_abi_version", "pp_footprint_bytes",
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
     "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
-    "pp_epoch_permute_local", "pp_propagate_store",
+    "pp_epoch_permute_local", "pp_propagate_store", "pp_next_batches_ev",
+    "pp_set_grid_limit",
 ]
 
 
@@ -122,6 +123,8 @@ def lib():
                 "pp_propagate": (st, [i64, i32, P, P, P, i32, P, P]),
                 "pp_epoch_permute_local": (st, [P, u64, i64, P]),
                 "pp_propagate_store": (st, [P, i32, P, P, P, P]),
+                "pp_next_batches_ev": (st, [P, i32, P, i64, P, P, P, P, P, P]),
+                "pp_set_grid_limit": (st, [P, i32]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -457,7 +457,8 @@ static cudaError_t launch_tma(const GatherArgs& a, bool pdl, int grid_per_sm, cu
     attr_set = true;
   }
   const int64_t tiles = ((a.B + tr - 1) / tr) * static_cast<int64_t>(a.nsteps);
-  const int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  if (a.max_ctas > 0 && a.max_ctas < cap) cap = a.max_ctas;
   const uint32_t grid = static_cast<uint32_t>(tiles < cap ? tiles : cap);
   return launch_ex(k_gather_tma<MODE, SH>, grid, pdl, smem, st, a, vpr, M, row_out_bytes, rec_in, tr);
 }
@@ -466,7 +467,8 @@ cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_
   if (a.tile_rows < 1 || a.tile_rows > kMaxTileRows) return cudaErrorInvalidValue;
   const int64_t tiles = ((a.B + a.tile_rows - 1) / a.tile_rows) * static_cast<int64_t>(a.nsteps);
   if (tiles <= 0) return cudaSuccess;
-  const int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  int64_t cap = static_cast<int64_t>(a.num_sms) * grid_per_sm;
+  if (a.max_ctas > 0 && a.max_ctas < cap) cap = a.max_ctas;
   const uint32_t grid = static_cast<uint32_t>(tiles < cap ? tiles : cap);
   const bool sharded = a.W > 1;
   const int s_out = a.out_dtype == kF32 ? 4 : 2;

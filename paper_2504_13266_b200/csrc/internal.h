@@ -85,6 +85,7 @@ struct GatherArgs {
   int32_t tile_rows;        // batch rows per CTA tile (1..32)
   int32_t num_sms;
   int32_t l2_prefetch;      // 0 none, 1 L2::128B, 2 L2::256B load hint (PPLOAD_L2_PREFETCH)
+  int32_t max_ctas = 0;     // > 0: cap on the grid (pp_set_grid_limit: leave SMs to an overlapped consumer)
 };
 
 // One launch assembling a.nsteps steps.  pdl: launch with programmatic stream

@@ -102,6 +102,7 @@ struct pp_loader {
   // Measured on products (profiles/r1j_exp_prefetch.jsonl): full grid 1.002 ms/epoch,
   // 148-296 CTAs 0.972 ms, 64 CTAs 1.11-1.15 ms (the sort then outlasts the epoch).
   int prefetch_ctas = 296;
+  int max_ctas = 0;  // pp_set_grid_limit: cap on the gather grid (0 = the full persistent grid)
   // previous op on the loader stream (programmatic dependent launch is only used
   // between consecutive launches of the same kind within one epoch)
   enum { kLastNone = 0, kLastGather = 1, kLastLinear = 2 };
@@ -580,6 +581,13 @@ pp_status pp_set_stream(pp_loader* L, void* stream) {
   return PP_OK;
 }
 
+pp_status pp_set_grid_limit(pp_loader* L, int32_t max_ctas) {
+  if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
+  if (max_ctas < 0) return fail(PP_ERR_INVALID, "max_ctas must be >= 0");
+  L->max_ctas = max_ctas;
+  return PP_OK;
+}
+
 pp_status pp_debug_set_sort_bits_delta(pp_loader* L, int32_t delta) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   L->sort_bits_delta = delta;
@@ -719,8 +727,17 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
   return PP_OK;
 }
 
+// How a call orders itself against the consumer: a consumer stream (the call waits for the
+// work enqueued on it so far and makes its later work wait for the batch), or explicit
+// events (wait for `wait_ev` before writing `out`, record `ready_ev` when it is written).
+struct Handoff {
+  bool events = false;
+  cudaStream_t cons = nullptr;
+  cudaEvent_t wait_ev = nullptr, ready_ev = nullptr;
+};
+
 static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stride, int32_t* out_labels,
-                            int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
+                            int64_t* out_nodes, int32_t* rows, int32_t* n_done, const Handoff& ho) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1) return fail(PP_ERR_INVALID, "rows is NULL or n < 1");
@@ -739,11 +756,15 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
                 (long long)(L->B * L->rec_out));
   const bool vec = L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
   DevGuard g(L->dev);
-  cudaStream_t cons = static_cast<cudaStream_t>(consumer_stream);
-  const bool handoff = cons != L->stream;
+  cudaStream_t cons = ho.cons;
+  const bool handoff = !ho.events && cons != L->stream;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
+    L->last_kernel = pp_loader::kLastNone;
+  }
+  if (ho.events && ho.wait_ev) {  // WAR: the consumer's last use of `out`
+    PPL_CUDA(L, cudaStreamWaitEvent(L->stream, ho.wait_ev, 0));
     L->last_kernel = pp_loader::kLastNone;
   }
   if (L->files) {
@@ -763,6 +784,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
       PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
       PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
     }
+    if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
     L->last_kernel = pp_loader::kLastNone;
     L->cursor += nsteps;
     if (n_done) *n_done = static_cast<int32_t>(nsteps);
@@ -794,6 +816,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   a.tile_rows = L->tile_rows;
   a.num_sms = L->num_sms;
   a.l2_prefetch = L->l2_prefetch;
+  a.max_ctas = L->max_ctas;
   // Programmatic dependent launch only right after another gather of this epoch:
   // batches of one epoch are independent, and the first gather after a permute
   // or an event wait is fully serialised, so every gather sees a complete order.
@@ -803,11 +826,12 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   const bool remote = L->n_spill > 0 || L->desc.peers == PP_PEERS_IPC;
   if (vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && remote))) path = kPathTma;
   PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_kernel == pp_loader::kLastGather, L->grid_per_sm, L->stream));
-  L->last_kernel = handoff ? pp_loader::kLastNone : pp_loader::kLastGather;
+  L->last_kernel = (handoff || (ho.events && ho.ready_ev)) ? pp_loader::kLastNone : pp_loader::kLastGather;
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
     PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
   }
+  if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
   for (int64_t i = 0; i < nsteps; ++i) {
     const int64_t s = a.first_pos + i * a.step_stride;
     rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - s)));
@@ -819,12 +843,26 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
 
 pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* out_nodes, int32_t* rows,
                         void* consumer_stream) {
-  return next_steps(L, 1, out, 0, out_labels, out_nodes, rows, nullptr, consumer_stream);
+  Handoff ho;
+  ho.cons = static_cast<cudaStream_t>(consumer_stream);
+  return next_steps(L, 1, out, 0, out_labels, out_nodes, rows, nullptr, ho);
 }
 
 pp_status pp_next_batches(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes, int32_t* out_labels,
                           int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
-  return next_steps(L, n, out, out_stride_bytes, out_labels, out_nodes, rows, n_done, consumer_stream);
+  Handoff ho;
+  ho.cons = static_cast<cudaStream_t>(consumer_stream);
+  return next_steps(L, n, out, out_stride_bytes, out_labels, out_nodes, rows, n_done, ho);
+}
+
+pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_stride_bytes, int32_t* out_labels,
+                             int64_t* out_nodes, int32_t* rows, int32_t* n_done, void* wait_event,
+                             void* ready_event) {
+  Handoff ho;
+  ho.events = true;
+  ho.wait_ev = static_cast<cudaEvent_t>(wait_event);
+  ho.ready_ev = static_cast<cudaEvent_t>(ready_event);
+  return next_steps(L, n, out, out_stride_bytes, out_labels, out_nodes, rows, n_done, ho);
 }
 
 pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,

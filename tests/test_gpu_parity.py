@@ -536,3 +536,40 @@ def test_device_resident_source(pp, layout):
         L.epoch_permute(4, 3)
         got = run_epoch(L, B, H, F, oracle.BF16)
         check_epoch(got, X.view(np.uint32), oracle.F32, hs, rs, H, F, oracle.epoch_order(4, N, 3), B, oracle.BF16)
+
+
+def test_event_double_buffer_matches_oracle(pp, tiny):
+    # pp_next_batches_ev: two buffers, per-buffer free / ready events, a consumer stream that copies
+    # each batch out after waiting on its ready event -- every batch equals the oracle's
+    X, bits = tiny
+    H, N, F = X.shape
+    B = 256
+    L = pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F, dtype=pp.PP_F32,
+                  batch_size=B, out_dtype=pp.PP_BF16)
+    cons = torch.cuda.Stream()
+    bufs = [torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for ev in ready + free:
+        ev.record(cons)
+    steps = oracle.num_steps(N, B)
+    got = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
+    L.epoch_permute(77, 1, cons)
+    rows = [0, 0]
+    with torch.cuda.stream(cons):
+        rows[0] = L.next_batches_ev(1, bufs[0], 0, None, None, free[0], ready[0])[0]
+        for t in range(steps):
+            b, nb = t % 2, (t + 1) % 2
+            if t + 1 < steps:
+                rows[nb] = L.next_batches_ev(1, bufs[nb], 0, None, None, free[nb], ready[nb])[0]
+            cons.wait_event(ready[b])
+            torch.cuda._sleep(20000)  # a slow consumer: the next batch must not overwrite this one early
+            got[t, :rows[b]].copy_(bufs[b][:rows[b]])
+            free[b].record(cons)
+    torch.cuda.synchronize()
+    order = oracle.epoch_order(77, N, 1)
+    for t in range(steps):
+        want, _, _ = oracle.batch(bits, oracle.F32, N * F, F, H, F, order, B, 1, t, 0, oracle.BF16)
+        assert np.array_equal(got[t, :want.shape[0]].cpu().view(torch.int16).numpy().view(np.uint16), want), t
+    assert L.next_batches_ev(1, bufs[0], 0) == []
+    L.close()
