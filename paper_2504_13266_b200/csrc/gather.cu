@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -500,6 +501,105 @@ cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_
   const uint64_t M = ((1ull << 40) + HF - 1) / HF;
   if (sharded) return launch_ex(k_gather_scalar<true>, grid, pdl, 0, st, a, HF, M);
   return launch_ex(k_gather_scalar<false>, grid, pdl, 0, st, a, HF, M);
+}
+
+// ---- DMA-staged assembly (chunk reshuffling over host-resident rows) -----------
+// The batch's records were DMA'd by the copy engines, in batch order, into a device
+// staging area (one cudaMemcpyAsync per run of consecutive rows); this kernel casts
+// staging record j into out row j and writes node ids / labels from the order.
+template <int MODE>
+__global__ void k_stage_cast(const uint8_t* __restrict__ stage, int64_t rec_stride, int32_t rows, uint32_t vpr,
+                             int64_t row_out_bytes, uint8_t* __restrict__ out, const uint32_t* __restrict__ order,
+                             const int64_t* __restrict__ node_set, const int32_t* __restrict__ labels,
+                             int32_t* __restrict__ out_labels, int64_t* __restrict__ out_nodes) {
+  constexpr int kInBytes = (MODE == kModeCopy) ? 16 : 32;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t j = tid; j < rows; j += nthr) {
+    const uint64_t o = order[j];
+    const int64_t id = node_set != nullptr ? node_set[o] : static_cast<int64_t>(o);
+    if (out_nodes) out_nodes[j] = id;
+    if (out_labels) out_labels[j] = labels[id];
+  }
+  const int64_t total = static_cast<int64_t>(rows) * vpr;
+  for (int64_t e = tid; e < total; e += nthr) {
+    const int64_t r = e / vpr, c = e - r * vpr;
+    const uint8_t* src = stage + r * rec_stride + c * kInBytes;
+    const uint4 x0 = ld_stream(src);
+    uint4 y = x0;
+    if (MODE != kModeCopy) {
+      const uint4 x1 = ld_stream(src + 16);
+      y = MODE == kModeBF16 ? make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y),
+                                         pack_bf16(x1.z, x1.w))
+                            : make_uint4(pack_f16(x0.x, x0.y), pack_f16(x0.z, x0.w), pack_f16(x1.x, x1.y),
+                                         pack_f16(x1.z, x1.w));
+    }
+    st_vec(out + r * row_out_bytes + c * 16, y);
+  }
+}
+
+// Scalar variant (records that rule out 16-byte vectors).
+__global__ void k_stage_cast_scalar(const uint8_t* __restrict__ stage, int64_t rec_stride, int32_t rows, int32_t HF,
+                                    int32_t in_dtype, int32_t out_dtype, uint8_t* __restrict__ out,
+                                    const uint32_t* __restrict__ order, const int64_t* __restrict__ node_set,
+                                    const int32_t* __restrict__ labels, int32_t* __restrict__ out_labels,
+                                    int64_t* __restrict__ out_nodes) {
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t j = tid; j < rows; j += nthr) {
+    const uint64_t o = order[j];
+    const int64_t id = node_set != nullptr ? node_set[o] : static_cast<int64_t>(o);
+    if (out_nodes) out_nodes[j] = id;
+    if (out_labels) out_labels[j] = labels[id];
+  }
+  const int s_in = in_dtype == kF32 ? 4 : 2, s_out = out_dtype == kF32 ? 4 : 2;
+  const int64_t total = static_cast<int64_t>(rows) * HF;
+  for (int64_t e = tid; e < total; e += nthr) {
+    const int64_t r = e / HF, i = e - r * HF;
+    const uint8_t* src = stage + r * rec_stride + i * s_in;
+    uint8_t* dst = out + (r * HF + i) * s_out;
+    if (s_in == 4) {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
+      if (out_dtype == kBF16)
+        *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(__uint_as_float(x));
+      else if (out_dtype == kF16)
+        *reinterpret_cast<__half*>(dst) = __float2half_rn(__uint_as_float(x));
+      else
+        *reinterpret_cast<uint32_t*>(dst) = x;
+    } else {
+      *reinterpret_cast<uint16_t*>(dst) = __ldg(reinterpret_cast<const unsigned short*>(src));
+    }
+  }
+}
+
+cudaError_t launch_stage_cast(const uint8_t* stage, int64_t rec_stride, int32_t rows, int32_t HF, int32_t in_dtype,
+                              int32_t out_dtype, bool vec, uint8_t* out, const uint32_t* order,
+                              const int64_t* node_set, const int32_t* labels, int32_t* out_labels, int64_t* out_nodes,
+                              cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int s_out = out_dtype == kF32 ? 4 : 2;
+  const int64_t row_out_bytes = static_cast<int64_t>(HF) * s_out;
+  if (vec) {
+    const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
+    const int64_t total = static_cast<int64_t>(rows) * vpr;
+    const uint32_t grid = static_cast<uint32_t>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    const int mode = (in_dtype == out_dtype) ? kModeCopy : (out_dtype == kBF16 ? kModeBF16 : kModeF16);
+    if (mode == kModeBF16)
+      k_stage_cast<kModeBF16><<<grid, 256, 0, st>>>(stage, rec_stride, rows, vpr, row_out_bytes, out, order, node_set,
+                                                      labels, out_labels, out_nodes);
+    else if (mode == kModeF16)
+      k_stage_cast<kModeF16><<<grid, 256, 0, st>>>(stage, rec_stride, rows, vpr, row_out_bytes, out, order, node_set,
+                                                     labels, out_labels, out_nodes);
+    else
+      k_stage_cast<kModeCopy><<<grid, 256, 0, st>>>(stage, rec_stride, rows, vpr, row_out_bytes, out, order, node_set,
+                                                      labels, out_labels, out_nodes);
+  } else {
+    const int64_t total = static_cast<int64_t>(rows) * HF;
+    const uint32_t grid = static_cast<uint32_t>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    k_stage_cast_scalar<<<grid, 256, 0, st>>>(stage, rec_stride, rows, HF, in_dtype, out_dtype, out, order, node_set,
+                                              labels, out_labels, out_nodes);
+  }
+  return cudaGetLastError();
 }
 
 // ---- K10: synthetic fill (SURVEY.md §8(d) generators G / G16) ----------------

@@ -146,6 +146,13 @@ struct StorePropArgs {
 };
 cudaError_t launch_spmm_store(const StorePropArgs& a, cudaStream_t st);
 
+// ---- DMA-staged assembly (gather.cu): out row j = cast(stage record j) ----------
+// order: the step's order entries (positions -> node-set index or node id), for ids / labels.
+cudaError_t launch_stage_cast(const uint8_t* stage, int64_t rec_stride, int32_t rows, int32_t HF, int32_t in_dtype,
+                              int32_t out_dtype, bool vec, uint8_t* out, const uint32_t* order,
+                              const int64_t* node_set, const int32_t* labels, int32_t* out_labels, int64_t* out_nodes,
+                              cudaStream_t st);
+
 // ---- exchange copy (gather.cu) ----------------------------------------------
 // dst[r] = cast(src[r]) for rows [0, rows): fp32 records (pitch rec_stride) ->
 // 16-bit records (pitch xrec_stride), the gather's RNE cast.  HF % 8 == 0.

@@ -118,6 +118,13 @@ struct pp_loader {
   std::vector<int64_t> h_node_set;    // host copy of the node set (empty: identity)
   // compact store (desc.store_set_only): records are node-set positions, not node ids
   bool compact = false;
+  // DMA-staged assembly for host-resident rows under chunk reshuffling (the paper's chunk
+  // transfer): runs of consecutive rows are moved by the copy engines
+  int dma_mode = 0;              // PPLOAD_SPILL_PATH: 0 auto (chunk >= dma_min_chunk), 1 always, 2 never
+  int64_t dma_min_chunk = 64;    // PPLOAD_DMA_MIN_CHUNK
+  bool dma_epoch = false;        // the current epoch uses it
+  uint32_t* h_order_pin = nullptr;  // pinned host copy of the order (run planning)
+  uint8_t* d_stage = nullptr;       // [B] records, batch order
   uint64_t epoch_id = 0;              // bumped by every permute / seek (invalidates staged steps)
 
   bool permuted = false, poisoned = false;
@@ -144,6 +151,8 @@ void release(pp_loader* L) {
   if (!L) return;
   if (L->stream) cudaStreamSynchronize(L->stream);
   if (L->files) file_tier_close(L->files);
+  if (L->h_order_pin) cudaFreeHost(L->h_order_pin);
+  cudaFree(L->d_stage);
   for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(L->d_store);
   cudaFree(L->d_xstore);
@@ -502,6 +511,10 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   if (const char* e = getenv("PPLOAD_L2_PREFETCH")) L->l2_prefetch = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("PPLOAD_PREFETCH_CTAS")) L->prefetch_ctas = std::max(0, atoi(e));
   if (const char* e = getenv("PPLOAD_GATHER")) L->gather_mode = !strcmp(e, "ldg") ? 1 : !strcmp(e, "tma") ? 2 : 0;
+  if (const char* e = getenv("PPLOAD_SPILL_PATH")) L->dma_mode = !strcmp(e, "dma") ? 1 : !strcmp(e, "kernel") ? 2 : 0;
+  if (const char* e = getenv("PPLOAD_DMA_MIN_CHUNK")) L->dma_min_chunk = std::max<long long>(1, atoll(e));
+  if (L->n_spill > 0 && desc->node_set && L->h_node_set.empty())  // run planning of the DMA path
+    L->h_node_set.assign(desc->node_set, desc->node_set + L->N);
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
   L->linked = (L->W == 1) || files;
@@ -646,6 +659,7 @@ pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, voi
     PPL_CUDA(L, cudaStreamWaitEvent(user, L->ev_out, 0));
   }
   L->local = true;
+  L->dma_epoch = false;
   L->steps = L->desc.drop_last ? L->local_rows / L->B : (L->local_rows + L->B - 1) / L->B;
   L->last_kernel = pp_loader::kLastNone;
   L->permuted = true;
@@ -695,6 +709,16 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
       L->poisoned = true;
       return fail(PP_ERR_OOM, "storage tier: %s", err.c_str());
     }
+  }
+  L->dma_epoch = L->W == 1 && L->n_spill > 0 && !L->files &&
+                 (L->dma_mode == 1 || (L->dma_mode == 0 && chunk >= L->dma_min_chunk));
+  if (L->dma_epoch) {  // the run planner needs the order on the host
+    if (!L->h_order_pin && cudaHostAlloc(&L->h_order_pin, L->N * 4, cudaHostAllocDefault) != cudaSuccess)
+      return fail(PP_ERR_OOM, "pinned order copy");
+    if (!L->d_stage && cudaMalloc(&L->d_stage, static_cast<size_t>(L->B * L->rec_stride)) != cudaSuccess)
+      return fail(PP_ERR_OOM, "DMA staging");
+    PPL_CUDA(L, cudaMemcpyAsync(L->h_order_pin, L->d_order, L->N * 4, cudaMemcpyDeviceToHost, L->stream));
+    PPL_CUDA(L, cudaStreamSynchronize(L->stream));
   }
   L->local = false;
   L->steps = L->steps_global;
@@ -786,6 +810,44 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
     }
     if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
     L->last_kernel = pp_loader::kLastNone;
+    L->cursor += nsteps;
+    if (n_done) *n_done = static_cast<int32_t>(nsteps);
+    return PP_OK;
+  }
+  if (L->dma_epoch) {
+    // chunk reshuffling over host-resident rows: one copy-engine DMA per run of consecutive
+    // records (pinned spill -> staging, or HBM -> staging), then a cast of the staged batch
+    const bool vec = L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const int64_t p0 = (L->cursor + i) * L->B;
+      const int32_t nr = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - p0)));
+      auto row_of = [&](int32_t j) -> int64_t {
+        const uint32_t o = L->h_order_pin[p0 + j];
+        return (L->compact || L->h_node_set.empty()) ? static_cast<int64_t>(o) : L->h_node_set[o];
+      };
+      auto src_of = [&](int64_t r) -> const uint8_t* {
+        return r < L->n_hbm ? L->d_store + r * L->rec_stride : L->h_spill + (r - L->n_hbm) * L->rec_stride;
+      };
+      for (int32_t j = 0; j < nr;) {
+        const int64_t r0 = row_of(j);
+        int32_t e = j + 1;
+        while (e < nr && row_of(e) == r0 + (e - j) && ((r0 + (e - j) < L->n_hbm) == (r0 < L->n_hbm))) ++e;
+        PPL_CUDA(L, cudaMemcpyAsync(L->d_stage + static_cast<int64_t>(j) * L->rec_stride, src_of(r0),
+                                    static_cast<size_t>(e - j) * L->rec_stride, cudaMemcpyDefault, L->stream));
+        j = e;
+      }
+      PPL_CUDA(L, launch_stage_cast(L->d_stage, L->rec_stride, nr, L->HF, L->in_dtype, L->out_dtype, vec,
+                                    static_cast<uint8_t*>(out) + i * out_stride, L->d_order + p0, L->d_node_set,
+                                    L->d_labels, out_labels ? out_labels + i * L->B : nullptr,
+                                    out_nodes ? out_nodes + i * L->B : nullptr, L->stream));
+      rows[i] = nr;
+    }
+    L->last_kernel = pp_loader::kLastNone;
+    if (handoff) {
+      PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
+      PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
+    }
+    if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
     L->cursor += nsteps;
     if (n_done) *n_done = static_cast<int32_t>(nsteps);
     return PP_OK;

@@ -117,6 +117,19 @@ if "papers100M-labelled" in which:
                 node_set=S)
 if "mag240m-1r" in which:
     measure("mag240m-1r", 25_000_000, 4, 768, 8192, 1, pp.PP_F16, pp.PP_F16, epochs=3)
+if "host-cr" in which:
+    # chunk reshuffling over a host-resident store: copy-engine DMA of whole runs (default for
+    # c >= 64) vs the zero-copy bulk-copy kernel (PPLOAD_SPILL_PATH=kernel)
+    peak = dma_peak()
+    print(json.dumps({"pcie_dma_h2d_GBs": peak}), flush=True)
+    for path in ("dma", "kernel"):
+        os.environ["PPLOAD_SPILL_PATH"] = path
+        measure(f"products-host-c8192-{path}", 2_449_029, 4, 100, 8192, 8192, pp.PP_F32, pp.PP_BF16, budget=-1,
+                epochs=3, bound="pcie", pcie_peak=peak)
+        n = 4_000_000
+        measure(f"igb-large-scaled-c4096-{path}", n, 3, 1024, 4096, 4096, pp.PP_F32, pp.PP_BF16,
+                budget=int(0.138 * n) * 3 * 1024 * 4, epochs=2, bound="pcie", pcie_peak=peak)
+    os.environ.pop("PPLOAD_SPILL_PATH")
 if "igb-large-scaled" in which:
     peak = dma_peak()
     print(json.dumps({"pcie_dma_h2d_GBs": peak}), flush=True)

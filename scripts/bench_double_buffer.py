@@ -51,6 +51,7 @@ def step(x, y):
             p.grad = None
 
 
+CHUNK = int(os.environ.get("DB_CHUNK", "1"))  # 1: SGD-RR; c > 1: chunk reshuffling (host rows then move by DMA)
 PLACEMENT = os.environ.get("DB_PLACEMENT", "hbm")  # hbm: GPU-resident store; host: pinned host memory (UVA)
 L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
               labels=labels_all.numpy().astype("int32"), hbm_budget_bytes=-1 if PLACEMENT == "host" else 0)
@@ -64,7 +65,7 @@ loader_stream = torch.cuda.Stream()
 
 def epoch_serial(e):
     L.set_stream(cons)  # the loader enqueues on the consumer's stream: no overlap
-    L.epoch_permute(e, 1, cons)
+    L.epoch_permute(e, CHUNK, cons)
     with torch.cuda.stream(cons):
         for t in range(steps):
             rows = L.next_batch(bufs[0], labs[0], None, cons)
@@ -83,7 +84,7 @@ def epoch_double(e, ctas=0):
     # the gather grid so the consumer's kernels keep SMs while a batch is assembled.
     L.set_grid_limit(ctas)
     L.set_stream(loader_stream)
-    L.epoch_permute(e, 1, cons)
+    L.epoch_permute(e, CHUNK, cons)
     rows = [0, 0]
     with torch.cuda.stream(cons):
         rows[0] = L.next_batches_ev(1, bufs[0], 0, labs[0], None, free[0], ready[0])[0]
@@ -104,7 +105,7 @@ def epoch_loader(e, ctas=0):
     # the loader alone (no consumer step), for the loader's own epoch time at this grid size
     L.set_grid_limit(ctas)
     L.set_stream(loader_stream)
-    L.epoch_permute(e, 1, cons)
+    L.epoch_permute(e, CHUNK, cons)
     with torch.cuda.stream(cons):
         for t in range(steps):
             L.next_batches_ev(1, bufs[t % 2], 0, labs[t % 2], None, None, ready[t % 2])
@@ -135,10 +136,10 @@ for name, fn in (("loader", epoch_loader), (f"loader_{CTAS}ctas", lambda e: epoc
                  ("compute", epoch_compute), ("serial", epoch_serial), ("double", epoch_double),
                  (f"double_{CTAS}ctas", lambda e: epoch_double(e, CTAS))):
     res[name] = timeit(fn)
-    print(json.dumps({"placement": PLACEMENT, "mode": name, "ms_per_epoch": res[name],
+    print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "mode": name, "ms_per_epoch": res[name],
                       "nodes_per_s": N / res[name] * 1e3}), flush=True)
 best = min(res["double"], res[f"double_{CTAS}ctas"])
-print(json.dumps({"placement": PLACEMENT, "double_buffer_speedup": res["serial"] / best,
+print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "double_buffer_speedup": res["serial"] / best,
                   "loader_hidden_fraction": (res["serial"] - best) / max(1e-9, res["serial"] - res["compute"]),
                   "paper": "1.33x GPU-resident (PAPER.md:441), 1.9x host-resident (PAPER.md:345), RTX A6000"}), flush=True)
 L.close()
