@@ -126,7 +126,14 @@ typedef struct {
                                beyond it spill to pinned mapped host memory.
                                0 => (free HBM - 2 GiB reserve); < 0 => all
                                rows in host memory (the paper's host
-                               placement).  W > 1 requires no spill. */
+                               placement).  W > 1 requires no spill.
+                               Host-resident rows are read zero-copy by the
+                               gather kernel; under chunk reshuffling
+                               (chunk >= 64, PPLOAD_DMA_MIN_CHUNK) each step's
+                               runs of consecutive records are moved by the
+                               copy engines instead (one cudaMemcpyAsync per
+                               run) and cast on the GPU
+                               (PPLOAD_SPILL_PATH=dma|kernel forces a path). */
   int32_t world_size;       /* W >= 1 */
   int32_t rank;             /* 0 <= r < W */
   pp_peers peers;           /* PP_PEERS_NONE iff W == 1 (file loaders: always
