@@ -64,6 +64,11 @@ constexpr int kABytes = kTileM * kKPad * 2;  // 32 KB per A stage
 constexpr int kStages = PPL_LIN_STAGES;  // A-tile stages
 constexpr int kStageBytes = 32 * 128;  // epilogue staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
 constexpr int kEpiBufs = PPL_LIN_EPIBUFS;  // staging buffers per epilogue warp
+#ifndef PPL_LIN_GROUP
+#define PPL_LIN_GROUP 1
+#endif
+constexpr int kEpiGroup = PPL_LIN_GROUP;   // slices staged per fence + TMA issue round
+static_assert(kEpiBufs % kEpiGroup == 0 && kEpiBufs / kEpiGroup >= 1, "staging buffers per group");
 #ifndef PPL_LIN_PFDIST
 #define PPL_LIN_PFDIST 1
 #endif
@@ -441,40 +446,39 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           if (a.z_elem == 2) PPL_TMEM_LD32(trow + c0 + 32, (v + 32));
         };
         if (c_lo < c_end) ld_slice(c_lo);
+        // kEpiGroup slices are staged per fence.proxy.async + TMA issue round (the fence waits
+        // for the staging stores to land, so grouping amortises that wait); one bulk group per round
 #pragma unroll 1
-        for (int c0 = c_lo; c0 < c_end; c0 += cols_per_slice, ++slice) {
-          uint8_t* sb = sbuf + (slice % kEpiBufs) * kStageBytes;
-          uint8_t* my = sb + lane * 128;
-          // the bulk store issued from this buffer kEpiBufs slices ago must have read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
+        for (int g0 = c_lo; g0 < c_end; g0 += cols_per_slice * kEpiGroup) {
+          // the bulk stores issued from these buffers kEpiBufs / kEpiGroup rounds ago must have read them
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs / kEpiGroup - 1) : "memory");
           __syncwarp();
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (a.z_elem == 2) {
+          uint8_t* sbs[kEpiGroup];
+          int ng = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
-                  make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                             bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
-          } else {
+          for (int g = 0; g < kEpiGroup; ++g) {
+            const int c0 = g0 + g * cols_per_slice;
+            if (c0 >= c_end) break;
+            uint8_t* sb = sbuf + (slice % kEpiBufs) * kStageBytes;
+            ++slice;
+            sbs[g] = sb;
+            ++ng;
+            uint8_t* my = sb + lane * 128;
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (a.z_elem == 2) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
-                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-          if (c0 + cols_per_slice < c_end) ld_slice(c0 + cols_per_slice);
-          if (a.debug & 2) continue;
-          if (tma_rows) {
-            fence_async_smem();  // generic-proxy staging writes -> visible to the bulk-copy engine
-            __syncwarp();
-            if (lane == 0) {
-              asm volatile(
-                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                      zmap_addr),
-                  "r"(h * kUmmaN + c0), "r"(k), "r"(r0 + e * 32), "r"(static_cast<int>(step)), "r"(smem_addr(sb))
-                  : "memory");
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
-          } else {
+            if (c0 + cols_per_slice < c_end) ld_slice(c0 + cols_per_slice);
+            if ((a.debug & 2) || tma_rows) continue;
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < 8; ++it) {  // 4 rows x 128 contiguous bytes per instruction
@@ -488,6 +492,19 @@ __global__ void __launch_bounds__(kLinThreads, 1)
               }
             }
             __syncwarp();
+          }
+          if ((a.debug & 2) || !tma_rows) continue;
+          fence_async_smem();  // generic-proxy staging writes -> visible to the bulk-copy engine
+          __syncwarp();
+          if (lane == 0) {
+            for (int g = 0; g < ng; ++g)
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                      zmap_addr),
+                  "r"(h * kUmmaN + g0 + g * cols_per_slice), "r"(k), "r"(r0 + e * 32), "r"(static_cast<int>(step)),
+                  "r"(smem_addr(sbs[g]))
+                  : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
         if (dbg_lane) dbg_ts(a, i, 8 + 2 * h, 0);
