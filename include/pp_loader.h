@@ -173,10 +173,13 @@ typedef struct {
 } pp_loader_info;
 
 /* Create a loader.  Copies the hop data into a library-owned, node-major store
- * [local_rows, H, F] (HBM part + optional pinned-host spill), uploads
- * node_set / labels, and creates the loader stream.  Synchronous.
+ * [local_rows, H, F] (HBM part + optional pinned-host spill; only the node
+ * set's records with store_set_only; no store but the opened hop files with
+ * PP_MEM_FILES), uploads node_set / labels, and creates the loader stream.
+ * Synchronous.  *out is NULL on error.
  * Errors: PP_ERR_INVALID (null/out-of-range fields, node_set id out of range,
- * unsupported dtype pair, W > 1 with spill), PP_ERR_OOM, PP_ERR_CUDA. */
+ * unsupported dtype pair, IPC sharding with spill, unreadable / short hop
+ * files, store_set_only without a node set), PP_ERR_OOM, PP_ERR_CUDA. */
 pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out);
 
 /* Release everything the handle owns (store, spill, order, streams, peer
