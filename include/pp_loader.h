@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 4
+#define PP_ABI_VERSION 5
 
 /* Bytes of one rank's exported store handle (pp_export_store). */
 #define PP_IPC_HANDLE_BYTES 128
@@ -147,6 +147,16 @@ typedef struct {
                                in-memory source; batches are identical to the full
                                store's.  Not with pp_propagate_store (which needs
                                every node).  0: every node has a record. */
+  int32_t borrow_device_data; /* 1: hops.data is a device tensor already in the
+                               store layout (node-major [N][H][F], hop_stride = F,
+                               row_stride = H*F, H*F*elem a 16-B multiple,
+                               16-B aligned): the loader uses it in place instead
+                               of copying it (no second copy of GPU-resident hop
+                               features).  The caller keeps it alive until
+                               pp_loader_destroy; pp_fill_synthetic and
+                               pp_propagate_store write into it.  Needs W == 1,
+                               no store_set_only and the whole store in HBM,
+                               else PP_ERR_INVALID.  0: copy (default). */
 } pp_loader_desc;
 
 /* Read-only facts about a loader (pp_loader_query). */

@@ -84,7 +84,7 @@ def pp_footprint_bytes(num_nodes, feat_dim, elem_bytes, num_ops, num_hops_R) -> 
 def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_dim, hop_stride=0, row_stride=0,
                      dtype=PP_F32, node_set=None, labels=None, batch_size, out_dtype=PP_BF16, drop_last=False,
                      hbm_budget_bytes=0, world_size=1, rank=0, peers=PP_PEERS_NONE, device=0, files=None,
-                     store_set_only=False):
+                     store_set_only=False, borrow_device_data=False):
     """pp_loader_create(desc) -> handle.  ``data`` is a numpy array (host) or a torch CUDA tensor
     (device) of the hop matrices with the given element strides; None allocates the store only.
     ``files``: H hop file paths (raw [N][F] of dtype each) -> the storage tier (PP_MEM_FILES)."""
@@ -128,6 +128,7 @@ def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_
     d.peers = peers
     d.device = device
     d.store_set_only = int(store_set_only)
+    d.borrow_device_data = int(borrow_device_data)
     h = ctypes.c_void_p()
     _check(lib().pp_loader_create(ctypes.byref(d), ctypes.byref(h)), "pp_loader_create")
     return h

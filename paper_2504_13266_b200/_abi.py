@@ -58,6 +58,7 @@ class pp_loader_desc(ctypes.Structure):
         ("peers", ctypes.c_int),
         ("device", ctypes.c_int32),
         ("store_set_only", ctypes.c_int32),
+        ("borrow_device_data", ctypes.c_int32),
     ]
 
 

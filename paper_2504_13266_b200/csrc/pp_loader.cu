@@ -64,6 +64,7 @@ struct pp_loader {
   bool vector_path = true;
 
   uint8_t* d_store = nullptr;
+  bool borrowed = false;        // d_store is the caller's buffer (desc.borrow_device_data)
   uint8_t* h_spill = nullptr;
   uint8_t* d_spill = nullptr;  // device alias of h_spill
   uint8_t* d_xstore = nullptr;  // exchange copy: HBM rows cast to out_dtype, read by the peers (W > 1)
@@ -154,7 +155,7 @@ void release(pp_loader* L) {
   if (L->h_order_pin) cudaFreeHost(L->h_order_pin);
   cudaFree(L->d_stage);
   for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
-  cudaFree(L->d_store);
+  if (!L->borrowed) cudaFree(L->d_store);
   cudaFree(L->d_xstore);
   if (L->h_spill) cudaFreeHost(L->h_spill);
   cudaFree(L->d_node_set);
@@ -451,13 +452,25 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (budget < 0) budget = 0;
   }
   L->n_hbm = files ? 0 : budget < 0 ? 0 : std::min<int64_t>(L->local_rows, budget / L->rec_stride);
+  if (desc->borrow_device_data && desc->hbm_budget_bytes == 0) L->n_hbm = L->local_rows;  // nothing to allocate
   if (files) L->local_rows = 0;
   L->n_spill = L->local_rows - L->n_hbm;
   if (L->W > 1 && L->n_spill > 0 && desc->peers == PP_PEERS_IPC)
     return bail(fail(PP_ERR_INVALID, "sharded (IPC) loaders need the whole shard in HBM (%lld rows spill)",
                      (long long)L->n_spill));
 
-  if (L->n_hbm > 0 && cudaMalloc(&L->d_store, static_cast<size_t>(L->n_hbm * L->rec_stride)) != cudaSuccess)
+  if (desc->borrow_device_data) {
+    // the caller's node-major device tensor IS the store (no copy; it must outlive the loader)
+    if (desc->hops.where != PP_MEM_DEVICE || !desc->hops.data || L->W != 1 || L->compact || files ||
+        desc->hops.hop_stride != L->F || desc->hops.row_stride != L->HF || L->rec_stride != L->rec_in ||
+        reinterpret_cast<uintptr_t>(desc->hops.data) % 16 != 0 || L->n_hbm != L->local_rows)
+      return bail(fail(PP_ERR_INVALID,
+                       "borrow_device_data needs a 16-B aligned node-major device tensor [N][H][F] with H*F*elem a "
+                       "16-B multiple, W == 1, no node-set compaction, and no HBM budget below the store"));
+    L->d_store = static_cast<uint8_t*>(const_cast<void*>(desc->hops.data));
+    L->borrowed = true;
+  }
+  if (!L->borrowed && L->n_hbm > 0 && cudaMalloc(&L->d_store, static_cast<size_t>(L->n_hbm * L->rec_stride)) != cudaSuccess)
     return bail(fail(PP_ERR_OOM, "cudaMalloc of the %lld-byte HBM store failed", (long long)(L->n_hbm * L->rec_stride)));
   if (L->n_spill > 0) {
     if (cudaHostAlloc(&L->h_spill, static_cast<size_t>(L->n_spill * L->rec_stride),
@@ -471,7 +484,7 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (e == cudaSuccess && L->n_spill > 0)
       e = copy_in_compact(L, desc->hops, desc->node_set, L->n_hbm, L->n_spill, L->h_spill, true);
     if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
-  } else if (desc->hops.data && !files) {
+  } else if (desc->hops.data && !files && !L->borrowed) {
     cudaError_t e = copy_in(L, desc->hops, 0, L->n_hbm, L->d_store);
     if (e == cudaSuccess && L->n_spill > 0) e = copy_in(L, desc->hops, L->n_hbm, L->n_spill, L->h_spill);
     if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));

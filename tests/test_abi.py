@@ -52,7 +52,7 @@ def _header_define(name):
 
 
 def test_abi_version_and_footprint(pp):
-    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 4
+    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 5
     assert pp.IPC_HANDLE_BYTES == _header_define("PP_IPC_HANDLE_BYTES")
     # input expansion K(R+1)x: 400 GB at R = 3, K = 1 -> 1.6 TB
     n = 100_000_000

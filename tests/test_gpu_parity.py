@@ -573,3 +573,36 @@ def test_event_double_buffer_matches_oracle(pp, tiny):
         assert np.array_equal(got[t, :want.shape[0]].cpu().view(torch.int16).numpy().view(np.uint16), want), t
     assert L.next_batches_ev(1, bufs[0], 0) == []
     L.close()
+
+
+def test_borrowed_device_store(pp, tiny):
+    # borrow_device_data: the caller's node-major device tensor is used in place (no copy);
+    # batches equal the oracle's, writes through the loader land in the caller's tensor
+    hops, bits = tiny
+    H, N, F = hops.shape
+    B = 256
+    nm = torch.from_numpy(np.ascontiguousarray(hops.transpose(1, 0, 2))).cuda()  # [N, H, F] fp32
+    with pp.Loader(data=nm, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=F, row_stride=H * F, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16, borrow_device_data=True) as L:
+        order = oracle.epoch_order(12, N, 1)
+        L.epoch_permute(12, 1)
+        out = torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda")
+        for t in range(oracle.num_steps(N, B)):
+            rows = L.next_batch(out)
+            torch.cuda.synchronize()
+            want, _, _ = oracle.batch(bits, oracle.F32, N * F, F, H, F, order, B, 1, t, 0, oracle.BF16)
+            assert np.array_equal(out[:rows].cpu().view(torch.int16).numpy().view(np.uint16), want), t
+        # in place: the loader's store is the caller's tensor
+        L.fill_synthetic(2504)
+        torch.cuda.synchronize()
+        want = oracle.gen_rows(2504, oracle.F32, H, F, np.arange(5)).reshape(5, H * F)
+        assert np.array_equal(nm[:5].reshape(5, H * F).cpu().view(torch.int32).numpy().view(np.uint32), want)
+    # layouts that cannot be borrowed are refused
+    with pytest.raises(pp.PPError) as ei:
+        pp.Loader(data=torch.from_numpy(hops).cuda(), num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F,
+                  row_stride=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16, borrow_device_data=True)
+    assert ei.value.status == pp.PP_ERR_INVALID
+    with pytest.raises(pp.PPError) as ei:  # host data
+        pp.Loader(data=hops, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F, dtype=pp.PP_F32,
+                  batch_size=B, out_dtype=pp.PP_BF16, borrow_device_data=True)
+    assert ei.value.status == pp.PP_ERR_INVALID
