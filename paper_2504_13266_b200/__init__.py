@@ -281,6 +281,10 @@ class Loader:
     def __init__(self, **desc):
         self.h = pp_loader_create(**desc)
         self.info = pp_loader_query(self.h)
+        self.info_hops = (desc["num_hops"], desc["feat_dim"])
+        self._batch_size = desc["batch_size"]
+        self._out_dtype = _dtype(desc.get("out_dtype", PP_BF16))
+        self._device = desc.get("device", 0)
         # per-batch hot path: the C entry point and the out-parameter bound once
         self._next = lib().pp_next_batch
         self._rows = ctypes.c_int32()
@@ -348,6 +352,52 @@ class Loader:
 
     def query(self):
         return pp_loader_query(self.h)
+
+    def epoch(self, seed, chunk=1, depth=2, labels=False, nodes=False, consumer_stream=None):
+        """Iterate one epoch with the paper's double buffer: ``depth`` batch
+        buffers, batch t+1.. assembled on the loader stream while the consumer works on batch t.
+
+        Yields ``(x, y, v)`` per step: ``x`` the [rows, H, F] batch, ``y`` int32 labels or None,
+        ``v`` int64 node ids or None -- views into the ring, valid until the consumer's work
+        enqueued on ``consumer_stream`` (default: torch's current stream) after the yield.
+        Ordering is by per-buffer events (pp_next_batches_ev); bookkeeping only, no compute."""
+        import torch
+
+        H, F = self.info_hops
+        B = self._batch_size
+        dt = {PP_BF16: torch.bfloat16, PP_F16: torch.float16, PP_F32: torch.float32}[self._out_dtype]
+        dev = torch.device("cuda", self._device)
+        cons = consumer_stream if consumer_stream is not None else torch.cuda.current_stream(dev)
+        bufs = torch.empty((depth, B, H, F), dtype=dt, device=dev)
+        ys = torch.empty((depth, B), dtype=torch.int32, device=dev) if labels else None
+        vs = torch.empty((depth, B), dtype=torch.int64, device=dev) if nodes else None
+        ready = [torch.cuda.Event() for _ in range(depth)]
+        free = [torch.cuda.Event() for _ in range(depth)]
+        for ev in ready + free:  # torch creates events lazily: materialise them
+            ev.record(cons)
+        self.epoch_permute(seed, chunk, cons)
+        steps = pp_loader_query(self.h)["steps_per_epoch"]
+        rows = [0] * depth
+        issued = 0
+
+        def issue(t):
+            b = t % depth
+            r = self.next_batches_ev(1, bufs[b], 0, None if ys is None else ys[b], None if vs is None else vs[b],
+                                     free[b], ready[b])
+            rows[b] = r[0] if r else 0
+
+        while issued < min(depth - 1, steps):
+            issue(issued)
+            issued += 1
+        for t in range(steps):
+            if issued < steps:  # keep depth - 1 batches in flight ahead of the consumer
+                issue(issued)
+                issued += 1
+            b = t % depth
+            cons.wait_event(ready[b])
+            n = rows[b]
+            yield bufs[b, :n], (None if ys is None else ys[b, :n]), (None if vs is None else vs[b, :n])
+            free[b].record(cons)
 
     def fill_synthetic(self, data_seed):
         pp_fill_synthetic(self.h, data_seed)

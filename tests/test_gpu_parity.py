@@ -606,3 +606,34 @@ def test_borrowed_device_store(pp, tiny):
         pp.Loader(data=hops, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F, dtype=pp.PP_F32,
                   batch_size=B, out_dtype=pp.PP_BF16, borrow_device_data=True)
     assert ei.value.status == pp.PP_ERR_INVALID
+
+
+@pytest.mark.parametrize("depth,chunk", [(2, 1), (3, 64)])
+def test_epoch_iterator_double_buffer(pp, tiny, depth, chunk):
+    # Loader.epoch: the double-buffered iterator over pp_next_batches_ev; a slow consumer on the
+    # current stream copies each yielded batch out; everything equals the oracle
+    hops, bits = tiny
+    H, N, F = hops.shape
+    B = 256
+    lab = make_labels(3, N)
+    with pp.Loader(data=hops, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F, dtype=pp.PP_F32,
+                   labels=lab, batch_size=B, out_dtype=pp.PP_BF16) as L:
+        steps = oracle.num_steps(N, B)
+        got = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
+        gl = torch.empty((steps, B), dtype=torch.int32, device="cuda")
+        gv = torch.empty((steps, B), dtype=torch.int64, device="cuda")
+        n = []
+        for t, (x, y, v) in enumerate(L.epoch(21, chunk, depth=depth, labels=True, nodes=True)):
+            torch.cuda._sleep(20000)
+            got[t, :x.shape[0]].copy_(x)
+            gl[t, :x.shape[0]].copy_(y)
+            gv[t, :x.shape[0]].copy_(v)
+            n.append(x.shape[0])
+        torch.cuda.synchronize()
+        assert len(n) == steps
+        order = oracle.epoch_order(21, N, chunk)
+        for t in range(steps):
+            want, wl, wn = oracle.batch(bits, oracle.F32, N * F, F, H, F, order, B, 1, t, 0, oracle.BF16, lab)
+            assert n[t] == want.shape[0]
+            assert np.array_equal(got[t, :n[t]].cpu().view(torch.int16).numpy().view(np.uint16), want), t
+            assert np.array_equal(gl[t, :n[t]].cpu().numpy(), wl) and np.array_equal(gv[t, :n[t]].cpu().numpy(), wn)
