@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, chunk, xcast, q):
+def _worker(rank, world, port, chunk, xcast, q, compact=False):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PPLOAD_EXCHANGE_CAST=str(xcast[rank]))
     import numpy as np
@@ -36,13 +36,15 @@ def _worker(rank, world, port, chunk, xcast, q):
     try:
         H, N, F, B = 4, 6007, 64, 96
         X, hs, rs = hop_tensor(40, H, N, F)
+        S = np.random.default_rng(41).choice(N, size=2500, replace=False).astype(np.int64) if compact else None
         L = pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
-                      batch_size=B, out_dtype=pp.PP_BF16, world_size=world, rank=rank, peers=pp.PP_PEERS_IPC)
+                      batch_size=B, out_dtype=pp.PP_BF16, world_size=world, rank=rank, peers=pp.PP_PEERS_IPC,
+                      node_set=S, store_set_only=compact)
         has_x = L.query()["exchange_cast"]
         ppd.link_ipc(L)
         ppd.check_epoch_args(17, chunk)
         L.epoch_permute(17, chunk)
-        order = oracle.epoch_order(17, N, chunk)
+        order = oracle.epoch_order(17, N if S is None else S.shape[0], chunk, node_set=S)
         out = torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda")
         nodes = torch.empty(B, dtype=torch.int64, device="cuda")
         t, bad = 0, 0
@@ -55,7 +57,7 @@ def _worker(rank, world, port, chunk, xcast, q):
             t += 1
         dist.barrier()  # peers keep their stores alive until everyone is done
         L.close()
-        q.put((rank, bad, t == oracle.num_steps(N, B, world), has_x))
+        q.put((rank, bad, t == oracle.num_steps(order.shape[0], B, world), has_x))
     except Exception as e:  # pragma: no cover - reported through the queue
         q.put((rank, repr(e), False, None))
     finally:
@@ -64,8 +66,9 @@ def _worker(rank, world, port, chunk, xcast, q):
 
 # xcast: per-rank PPLOAD_EXCHANGE_CAST -- peers read the owner's cast exchange copy (1) or its fp32
 # records (0); mixed ranks exercise both in one epoch.  Batches are bit-identical either way.
-@pytest.mark.parametrize("chunk,xcast", [(1, (1, 1)), (64, (1, 1)), (1, (0, 0)), (64, (1, 0))])
-def test_ipc_two_processes_one_gpu(chunk, xcast):
+@pytest.mark.parametrize("chunk,xcast,compact", [(1, (1, 1), False), (64, (1, 1), False), (1, (0, 0), False),
+                                                 (64, (1, 0), False), (16, (1, 0), True)])
+def test_ipc_two_processes_one_gpu(chunk, xcast, compact):
     import torch.multiprocessing as mp
 
     import __graft_entry__ as ge
@@ -74,7 +77,7 @@ def test_ipc_two_processes_one_gpu(chunk, xcast):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, chunk, xcast, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, chunk, xcast, q, compact)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
