@@ -773,6 +773,112 @@ struct Handoff {
   cudaEvent_t wait_ev = nullptr, ready_ev = nullptr;
 };
 
+// The output slots of one next_steps call: step i goes to out + i*stride (labels / node
+// ids + i*B), rows[i] receives its row count.
+struct StepOut {
+  uint8_t* out;
+  int64_t stride;
+  int32_t* labels;
+  int64_t* nodes;
+  int32_t* rows;
+  bool vec;  // 16-byte aligned slots: the vector kernels apply
+};
+
+// Storage tier: each step's rows are read from the hop files, then assembled on the GPU.
+static pp_status enqueue_file_steps(pp_loader* L, int64_t nsteps, const StepOut& o) {
+  for (int64_t i = 0; i < nsteps; ++i) {
+    std::string err;
+    cudaError_t e = file_tier_step(L->files, L->cursor + i, L->in_dtype, L->out_dtype, L->d_labels, o.out + i * o.stride,
+                                   o.labels ? o.labels + i * L->B : nullptr, o.nodes ? o.nodes + i * L->B : nullptr,
+                                   L->stream, &o.rows[i], &err);
+    if (e == cudaErrorUnknown) {
+      L->poisoned = true;
+      return fail(PP_ERR_CUDA, "storage tier: %s", err.c_str());
+    }
+    if (e != cudaSuccess) return cuda_fail(L, e, "storage tier step");
+  }
+  L->last_kernel = pp_loader::kLastNone;
+  return PP_OK;
+}
+
+// Chunk reshuffling over host-resident rows: one copy-engine DMA per run of consecutive
+// records (pinned spill -> staging, or HBM -> staging), then a cast of the staged batch.
+static pp_status enqueue_dma_steps(pp_loader* L, int64_t nsteps, const StepOut& o) {
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const int64_t p0 = (L->cursor + i) * L->B;
+    const int32_t nr = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - p0)));
+    auto row_of = [&](int32_t j) -> int64_t {
+      const uint32_t v = L->h_order_pin[p0 + j];
+      return (L->compact || L->h_node_set.empty()) ? static_cast<int64_t>(v) : L->h_node_set[v];
+    };
+    auto src_of = [&](int64_t r) -> const uint8_t* {
+      return r < L->n_hbm ? L->d_store + r * L->rec_stride : L->h_spill + (r - L->n_hbm) * L->rec_stride;
+    };
+    for (int32_t j = 0; j < nr;) {
+      const int64_t r0 = row_of(j);
+      int32_t e = j + 1;
+      while (e < nr && row_of(e) == r0 + (e - j) && ((r0 + (e - j) < L->n_hbm) == (r0 < L->n_hbm))) ++e;
+      PPL_CUDA(L, cudaMemcpyAsync(L->d_stage + static_cast<int64_t>(j) * L->rec_stride, src_of(r0),
+                                  static_cast<size_t>(e - j) * L->rec_stride, cudaMemcpyDefault, L->stream));
+      j = e;
+    }
+    PPL_CUDA(L, launch_stage_cast(L->d_stage, L->rec_stride, nr, L->HF, L->in_dtype, L->out_dtype, o.vec,
+                                  o.out + i * o.stride, L->d_order + p0, L->d_node_set, L->d_labels,
+                                  o.labels ? o.labels + i * L->B : nullptr, o.nodes ? o.nodes + i * L->B : nullptr,
+                                  L->stream));
+    o.rows[i] = nr;
+  }
+  L->last_kernel = pp_loader::kLastNone;
+  return PP_OK;
+}
+
+// HBM / zero-copy host / peer rows: the gather kernels, all nsteps in one launch.
+static pp_status enqueue_gather_steps(pp_loader* L, int64_t nsteps, const StepOut& o, bool pdl_ok) {
+  GatherArgs a{};
+  a.order = L->d_order;
+  a.node_set = L->compact ? nullptr : L->d_node_set;  // compact: rows are node-set positions
+  a.out_ids = L->compact ? L->d_node_set : nullptr;
+  a.labels = L->d_labels;
+  // global epoch: step t of rank r = positions [tWB + rB, ...) of the shared order;
+  // local epoch: step t = positions [tB, ...) of this rank's own order
+  a.N = L->local ? L->local_rows : L->N;
+  a.first_pos = L->local ? L->cursor * L->B : L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
+  a.step_stride = L->local ? L->B : L->B * L->W;
+  a.B = static_cast<int32_t>(L->B);
+  a.nsteps = static_cast<int32_t>(nsteps);
+  a.out = o.out;
+  a.out_stride = o.stride;
+  a.out_labels = o.labels;
+  a.out_nodes = o.nodes;
+  a.W = L->W;
+  for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = L->shards[i];
+  a.rec_stride = L->rec_stride;
+  a.xrec_stride = L->xrec_stride;
+  a.HF = L->HF;
+  a.in_dtype = L->in_dtype;
+  a.out_dtype = L->out_dtype;
+  a.tile_rows = L->tile_rows;
+  a.num_sms = L->num_sms;
+  a.l2_prefetch = L->l2_prefetch;
+  a.max_ctas = L->max_ctas;
+  int path = o.vec ? kPathVector : kPathScalar;
+  // auto: register-staged loads for HBM-resident stores (96 % of copy bandwidth measured);
+  // bulk copies when rows come over PCIe (2x the zero-copy LDG rate measured) or NVLink
+  const bool remote = L->n_spill > 0 || L->desc.peers == PP_PEERS_IPC;
+  if (o.vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && remote))) path = kPathTma;
+  // Programmatic dependent launch only right after another gather of this epoch: batches of
+  // one epoch are independent, and the first gather after a permute or an event wait is
+  // fully serialised, so every gather sees a complete order.
+  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_kernel == pp_loader::kLastGather, L->grid_per_sm, L->stream));
+  // the next gather may overlap this one unless an event record follows it (pdl_ok false)
+  L->last_kernel = pdl_ok ? pp_loader::kLastGather : pp_loader::kLastNone;
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const int64_t s0 = a.first_pos + i * a.step_stride;
+    o.rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - s0)));
+  }
+  return PP_OK;
+}
+
 static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stride, int32_t* out_labels,
                             int64_t* out_nodes, int32_t* rows, int32_t* n_done, const Handoff& ho) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
@@ -791,126 +897,32 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   if (nsteps > 1 && out_stride < L->B * L->rec_out)
     return fail(PP_ERR_INVALID, "out_stride_bytes %lld < one batch (%lld)", (long long)out_stride,
                 (long long)(L->B * L->rec_out));
-  const bool vec = L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
   DevGuard g(L->dev);
-  cudaStream_t cons = ho.cons;
-  const bool handoff = !ho.events && cons != L->stream;
-  if (handoff) {
-    PPL_CUDA(L, cudaEventRecord(L->ev_in, cons));  // WAR: earlier consumer work on `out`
+  // ---- consumer -> loader (WAR on `out`)
+  const bool handoff = !ho.events && ho.cons != L->stream;
+  if (handoff) {  // the consumer stream's work so far
+    PPL_CUDA(L, cudaEventRecord(L->ev_in, ho.cons));
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_in, 0));
     L->last_kernel = pp_loader::kLastNone;
   }
-  if (ho.events && ho.wait_ev) {  // WAR: the consumer's last use of `out`
+  if (ho.events && ho.wait_ev) {  // the consumer's last use of `out`
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, ho.wait_ev, 0));
     L->last_kernel = pp_loader::kLastNone;
   }
-  if (L->files) {
-    // storage tier: each step's rows are read from the hop files, then assembled on the GPU
-    for (int64_t i = 0; i < nsteps; ++i) {
-      std::string err;
-      cudaError_t e = file_tier_step(L->files, L->cursor + i, L->in_dtype, L->out_dtype, L->d_labels,
-                                     static_cast<uint8_t*>(out) + i * out_stride, out_labels ? out_labels + i * L->B : nullptr,
-                                     out_nodes ? out_nodes + i * L->B : nullptr, L->stream, &rows[i], &err);
-      if (e == cudaErrorUnknown) {
-        L->poisoned = true;
-        return fail(PP_ERR_CUDA, "storage tier: %s", err.c_str());
-      }
-      if (e != cudaSuccess) return cuda_fail(L, e, "storage tier step");
-    }
-    if (handoff) {
-      PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
-      PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
-    }
-    if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
-    L->last_kernel = pp_loader::kLastNone;
-    L->cursor += nsteps;
-    if (n_done) *n_done = static_cast<int32_t>(nsteps);
-    return PP_OK;
-  }
-  if (L->dma_epoch) {
-    // chunk reshuffling over host-resident rows: one copy-engine DMA per run of consecutive
-    // records (pinned spill -> staging, or HBM -> staging), then a cast of the staged batch
-    const bool vec = L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
-    for (int64_t i = 0; i < nsteps; ++i) {
-      const int64_t p0 = (L->cursor + i) * L->B;
-      const int32_t nr = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - p0)));
-      auto row_of = [&](int32_t j) -> int64_t {
-        const uint32_t o = L->h_order_pin[p0 + j];
-        return (L->compact || L->h_node_set.empty()) ? static_cast<int64_t>(o) : L->h_node_set[o];
-      };
-      auto src_of = [&](int64_t r) -> const uint8_t* {
-        return r < L->n_hbm ? L->d_store + r * L->rec_stride : L->h_spill + (r - L->n_hbm) * L->rec_stride;
-      };
-      for (int32_t j = 0; j < nr;) {
-        const int64_t r0 = row_of(j);
-        int32_t e = j + 1;
-        while (e < nr && row_of(e) == r0 + (e - j) && ((r0 + (e - j) < L->n_hbm) == (r0 < L->n_hbm))) ++e;
-        PPL_CUDA(L, cudaMemcpyAsync(L->d_stage + static_cast<int64_t>(j) * L->rec_stride, src_of(r0),
-                                    static_cast<size_t>(e - j) * L->rec_stride, cudaMemcpyDefault, L->stream));
-        j = e;
-      }
-      PPL_CUDA(L, launch_stage_cast(L->d_stage, L->rec_stride, nr, L->HF, L->in_dtype, L->out_dtype, vec,
-                                    static_cast<uint8_t*>(out) + i * out_stride, L->d_order + p0, L->d_node_set,
-                                    L->d_labels, out_labels ? out_labels + i * L->B : nullptr,
-                                    out_nodes ? out_nodes + i * L->B : nullptr, L->stream));
-      rows[i] = nr;
-    }
-    L->last_kernel = pp_loader::kLastNone;
-    if (handoff) {
-      PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
-      PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
-    }
-    if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
-    L->cursor += nsteps;
-    if (n_done) *n_done = static_cast<int32_t>(nsteps);
-    return PP_OK;
-  }
-  GatherArgs a{};
-  a.order = L->d_order;
-  a.node_set = L->compact ? nullptr : L->d_node_set;  // compact: rows are node-set positions
-  a.out_ids = L->compact ? L->d_node_set : nullptr;
-  a.labels = L->d_labels;
-  // global epoch: step t of rank r = positions [tWB + rB, ...) of the shared order;
-  // local epoch: step t = positions [tB, ...) of this rank's own order
-  a.N = L->local ? L->local_rows : L->N;
-  a.first_pos = L->local ? L->cursor * L->B : L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
-  a.step_stride = L->local ? L->B : L->B * L->W;
-  a.B = static_cast<int32_t>(L->B);
-  a.nsteps = static_cast<int32_t>(nsteps);
-  a.out = static_cast<uint8_t*>(out);
-  a.out_stride = out_stride;
-  a.out_labels = out_labels;
-  a.out_nodes = out_nodes;
-  a.W = L->W;
-  for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = L->shards[i];
-  a.rec_stride = L->rec_stride;
-  a.xrec_stride = L->xrec_stride;
-  a.HF = L->HF;
-  a.in_dtype = L->in_dtype;
-  a.out_dtype = L->out_dtype;
-  a.tile_rows = L->tile_rows;
-  a.num_sms = L->num_sms;
-  a.l2_prefetch = L->l2_prefetch;
-  a.max_ctas = L->max_ctas;
-  // Programmatic dependent launch only right after another gather of this epoch:
-  // batches of one epoch are independent, and the first gather after a permute
-  // or an event wait is fully serialised, so every gather sees a complete order.
-  int path = vec ? kPathVector : kPathScalar;
-  // auto: register-staged loads for HBM-resident stores (96 % of copy bandwidth measured);
-  // bulk copies when rows come over PCIe (2x the zero-copy LDG rate measured) or NVLink
-  const bool remote = L->n_spill > 0 || L->desc.peers == PP_PEERS_IPC;
-  if (vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && remote))) path = kPathTma;
-  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_kernel == pp_loader::kLastGather, L->grid_per_sm, L->stream));
-  L->last_kernel = (handoff || (ho.events && ho.ready_ev)) ? pp_loader::kLastNone : pp_loader::kLastGather;
+  // ---- the steps
+  StepOut o{static_cast<uint8_t*>(out), out_stride, out_labels, out_nodes, rows,
+            L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0)};
+  const bool signals = handoff || (ho.events && ho.ready_ev);  // an event record follows the steps
+  pp_status st = L->files ? enqueue_file_steps(L, nsteps, o)
+                 : L->dma_epoch ? enqueue_dma_steps(L, nsteps, o)
+                                : enqueue_gather_steps(L, nsteps, o, !signals);
+  if (st != PP_OK) return st;
+  // ---- loader -> consumer (RAW on `out`)
   if (handoff) {
     PPL_CUDA(L, cudaEventRecord(L->ev_out, L->stream));
-    PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
+    PPL_CUDA(L, cudaStreamWaitEvent(ho.cons, L->ev_out, 0));
   }
   if (ho.events && ho.ready_ev) PPL_CUDA(L, cudaEventRecord(ho.ready_ev, L->stream));
-  for (int64_t i = 0; i < nsteps; ++i) {
-    const int64_t s = a.first_pos + i * a.step_stride;
-    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - s)));
-  }
   L->cursor += nsteps;
   if (n_done) *n_done = static_cast<int32_t>(nsteps);
   return PP_OK;
