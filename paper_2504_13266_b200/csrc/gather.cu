@@ -31,7 +31,7 @@
 
 namespace ppl {
 
-constexpr int kMaxTileRows = 32;
+constexpr int kMaxTileRows = 128;  // small records use larger tiles (pp_loader picks tile_rows)
 constexpr int kGatherThreads = 256;
 constexpr int kUnroll = 4;
 constexpr int kMinBlocksPerSM = 4;  // caps registers at 64 -> 32 resident warps per SM
@@ -76,14 +76,39 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t e, uint64_t M) {
   return static_cast<uint32_t>((static_cast<uint64_t>(e) * M) >> 40);
 }
 
+// Tile t of a launch -> (step, first row j0, rows, first order position); rows <= 0: empty.
+struct TileCursor {
+  int64_t step, pos;
+  int j0, rows;
+};
+__device__ __forceinline__ TileCursor tile_cursor(const GatherArgs& a, int64_t tile, int64_t tiles_per_step,
+                                                  int64_t total_tiles, int tile_rows) {
+  TileCursor c{0, 0, 0, 0};
+  if (tile >= total_tiles) return c;
+  c.step = tile / tiles_per_step;
+  c.j0 = static_cast<int>(tile - c.step * tiles_per_step) * tile_rows;
+  const int64_t step_pos = a.first_pos + c.step * a.step_stride;
+  const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
+  c.rows = static_cast<int>(min(static_cast<int64_t>(tile_rows), nrows_step - c.j0));
+  c.pos = step_pos + c.j0;
+  return c;
+}
+
+// This thread's order[] entry of tile t (threads < rows), loaded a tile ahead of its use.
+__device__ __forceinline__ uint32_t prefetch_order(const GatherArgs& a, int64_t tile, int64_t tiles_per_step,
+                                                   int64_t total_tiles, int tile_rows) {
+  const TileCursor c = tile_cursor(a, tile, tiles_per_step, total_tiles, tile_rows);
+  return (c.rows > 0 && static_cast<int>(threadIdx.x) < c.rows) ? a.order[c.pos + threadIdx.x] : 0u;
+}
+
 // Resolve the tile's rows (threads 0..rows-1): source record pointer into
 // shared memory, labels / node ids out.
-template <bool SHARDED>
-__device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, int64_t step_pos, int j0,
-                                             int rows, const uint8_t** s_src) {
+// PF: `ord` is this row's order[] entry, fetched a tile ahead; otherwise it is loaded here.
+template <bool SHARDED, bool PF>
+__device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, int64_t step_pos, int j0, int rows,
+                                             uint32_t ord, const uint8_t** s_src) {
   if (threadIdx.x < rows) {
-    const int64_t p = step_pos + j0 + threadIdx.x;
-    uint64_t v = a.order[p];
+    uint64_t v = PF ? ord : a.order[step_pos + j0 + threadIdx.x];
     if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
     int owner = 0;
     uint64_t lr = v;
@@ -106,7 +131,10 @@ __device__ __forceinline__ void resolve_rows(const GatherArgs& a, int64_t step, 
 
 // Vector path: MODE bf16/f16 reads 32 B (8 fp32) and writes 16 B; copy mode
 // moves 16 B.  vpr = vector slots per row.
-template <int MODE, bool SHARDED>
+// PF: fetch the next tile's order[] entries one tile ahead (used with the larger tiles of
+// small records, where the order -> record round trip would dominate; for records >= 1 KB
+// the extra registers cost more than they save, r1z).
+template <int MODE, bool SHARDED, bool PF>
 __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
     k_gather_vec(const GatherArgs a, uint32_t vpr, uint64_t vpr_M, int64_t row_out_bytes) {
   __shared__ const uint8_t* s_src[2][kMaxTileRows];
@@ -118,14 +146,19 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
   const int64_t tiles_per_step = (a.B + kTileRows - 1) / kTileRows;
   const int64_t total_tiles = tiles_per_step * a.nsteps;
   int buf = 0;
+  // order[] entries of this CTA's next tile are loaded one tile ahead, so the order ->
+  // record dependency costs no extra memory round trip per tile (matters for small records)
+  uint32_t ord = PF ? prefetch_order(a, blockIdx.x, tiles_per_step, total_tiles, kTileRows) : 0u;
   for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const int64_t step = tile / tiles_per_step;
     const int j0 = static_cast<int>(tile - step * tiles_per_step) * kTileRows;
     const int64_t step_pos = a.first_pos + step * a.step_stride;
     const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
     const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), nrows_step - j0));
+    const uint32_t my_ord = ord;
+    if (PF) ord = prefetch_order(a, tile + gridDim.x, tiles_per_step, total_tiles, kTileRows);
     if (rows <= 0) continue;  // block-uniform; buf is not toggled
-    resolve_rows<SHARDED>(a, step, step_pos, j0, rows, s_src[buf]);
+    resolve_rows<SHARDED, PF>(a, step, step_pos, j0, rows, my_ord, s_src[buf]);
     __syncthreads();
     uint8_t* out_tile = a.out + step * a.out_stride + static_cast<int64_t>(j0) * row_out_bytes;
     const uint32_t nvec = static_cast<uint32_t>(rows) * vpr;
@@ -198,7 +231,7 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
     const int64_t nrows_step = min(static_cast<int64_t>(a.B), a.N - step_pos);
     const int rows = static_cast<int>(min(static_cast<int64_t>(kTileRows), nrows_step - j0));
     if (rows <= 0) continue;
-    resolve_rows<SHARDED>(a, step, step_pos, j0, rows, s_src[buf]);
+    resolve_rows<SHARDED, false>(a, step, step_pos, j0, rows, 0u, s_src[buf]);
     __syncthreads();
     uint8_t* out_tile = a.out + step * a.out_stride + static_cast<int64_t>(j0) * row_out_bytes;
     const uint32_t nel = static_cast<uint32_t>(rows) * HF;
@@ -490,7 +523,9 @@ cudaError_t launch_gather(const GatherArgs& a, int path, bool pdl, int grid_per_
     const uint32_t vpr = static_cast<uint32_t>(row_out_bytes / 16);
     const uint64_t M = ((1ull << 40) + vpr - 1) / vpr;
     if (static_cast<uint64_t>(kMaxTileRows) * vpr * vpr >= (1ull << 40)) return cudaErrorInvalidValue;
-#define PPL_GV(MODE, SH) return launch_ex(k_gather_vec<MODE, SH>, grid, pdl, 0, st, a, vpr, M, row_out_bytes)
+#define PPL_GV(MODE, SH)                                                                                 \
+  return a.tile_rows > 32 ? launch_ex(k_gather_vec<MODE, SH, true>, grid, pdl, 0, st, a, vpr, M, row_out_bytes) \
+                          : launch_ex(k_gather_vec<MODE, SH, false>, grid, pdl, 0, st, a, vpr, M, row_out_bytes)
     if (mode == kModeBF16) { if (sharded) PPL_GV(kModeBF16, true); else PPL_GV(kModeBF16, false); }
     else if (mode == kModeF16) { if (sharded) PPL_GV(kModeF16, true); else PPL_GV(kModeF16, false); }
     else { if (sharded) PPL_GV(kModeCopy, true); else PPL_GV(kModeCopy, false); }

@@ -512,7 +512,10 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
       cudaStreamCreateWithPriority(&L->pstream, cudaStreamNonBlocking, prefetch_priority()) != cudaSuccess)
     return bail(fail(PP_ERR_CUDA, "event creation"));
   cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, L->dev);
-  if (const char* e = getenv("PPLOAD_TILE_ROWS")) L->tile_rows = std::max(1, std::min(32, atoi(e)));
+  // rows per gather tile: 32 for records >= 1 KB (measured best, r1i); small records get up to 128
+  // rows so a tile still carries ~32 KB of loads per order round trip (r1z sweep)
+  while (L->tile_rows < 128 && L->tile_rows * L->rec_in < 32768) L->tile_rows *= 2;
+  if (const char* e = getenv("PPLOAD_TILE_ROWS")) L->tile_rows = std::max(1, std::min(128, atoi(e)));
   if (const char* e = getenv("PPLOAD_PDL")) L->pdl = atoi(e) != 0;
   if (const char* e = getenv("PPLOAD_GRID_PER_SM")) L->grid_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("PPLOAD_DEBUG_TIE_BITS")) {  // test knob: keep only the top n sub-key bits
