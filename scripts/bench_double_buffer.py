@@ -38,7 +38,18 @@ params = [W1, W2, W3]
 labels_all = torch.randint(0, C, (N,), dtype=torch.int64)
 
 
+GRAPH = os.environ.get("DB_GRAPH", "0") == "1"  # capture the consumer step in CUDA graphs (GPU-bound step)
+graphs = {}
+
+
 def step(x, y):
+    if GRAPH and x.shape[0] == B and (x.data_ptr(), y.data_ptr()) in graphs:
+        graphs[(x.data_ptr(), y.data_ptr())].replay()
+        return
+    _step(x, y)
+
+
+def _step(x, y):
     # x: [rows, H, F] bf16 batch, y: [rows] labels
     z = torch.bmm(x.transpose(0, 1), W1)             # [H, rows, D] per-hop linear
     h = torch.relu(z.transpose(0, 1).reshape(x.shape[0], H * D))
@@ -61,6 +72,26 @@ bufs = [torch.empty((B, H, F), dtype=torch.bfloat16, device=dev) for _ in range(
 labs = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(2)]
 cons = torch.cuda.Stream()
 loader_stream = torch.cuda.Stream()
+if GRAPH:  # one graph per (batch buffer, label buffer) pair; the ragged last batch runs eagerly
+    ylong = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(2)]
+    with torch.cuda.stream(cons):
+        for _ in range(3):  # warm-up (allocator, autograd) before capture
+            _step(bufs[0], ylong[0])
+    torch.cuda.synchronize()
+    for b in range(2):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cons):
+            ylong[b].copy_(labs[b])
+            _step(bufs[b], ylong[b])
+        graphs[(bufs[b].data_ptr(), labs[b].data_ptr())] = g
+    torch.cuda.synchronize()
+
+
+def step_b(b, rows):
+    if GRAPH and rows == B:
+        graphs[(bufs[b].data_ptr(), labs[b].data_ptr())].replay()
+    else:
+        _step(bufs[b][:rows], labs[b][:rows].long())
 
 
 def epoch_serial(e):
@@ -69,7 +100,7 @@ def epoch_serial(e):
     with torch.cuda.stream(cons):
         for t in range(steps):
             rows = L.next_batch(bufs[0], labs[0], None, cons)
-            step(bufs[0][:rows], labs[0][:rows].long())
+            step_b(0, rows)
 
 
 ready = [torch.cuda.Event() for _ in range(2)]
@@ -93,7 +124,7 @@ def epoch_double(e, ctas=0):
             if t + 1 < steps:
                 rows[nb] = L.next_batches_ev(1, bufs[nb], 0, labs[nb], None, free[nb], ready[nb])[0]
             cons.wait_event(ready[b])
-            step(bufs[b][:rows[b]], labs[b][:rows[b]].long())
+            step_b(b, rows[b])
             free[b].record(cons)
     L.set_grid_limit(0)
 
@@ -116,7 +147,7 @@ def epoch_loader(e, ctas=0):
 def epoch_compute(e):
     with torch.cuda.stream(cons):
         for t in range(steps):
-            step(bufs[0], labs[0].long())
+            step_b(0, B)
 
 
 def timeit(fn):
@@ -136,10 +167,10 @@ for name, fn in (("loader", epoch_loader), (f"loader_{CTAS}ctas", lambda e: epoc
                  ("compute", epoch_compute), ("serial", epoch_serial), ("double", epoch_double),
                  (f"double_{CTAS}ctas", lambda e: epoch_double(e, CTAS))):
     res[name] = timeit(fn)
-    print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "mode": name, "ms_per_epoch": res[name],
+    print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "graph": GRAPH, "mode": name, "ms_per_epoch": res[name],
                       "nodes_per_s": N / res[name] * 1e3}), flush=True)
 best = min(res["double"], res[f"double_{CTAS}ctas"])
-print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "double_buffer_speedup": res["serial"] / best,
+print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "graph": GRAPH, "double_buffer_speedup": res["serial"] / best,
                   "loader_hidden_fraction": (res["serial"] - best) / max(1e-9, res["serial"] - res["compute"]),
                   "paper": "1.33x GPU-resident (PAPER.md:441), 1.9x host-resident (PAPER.md:345), RTX A6000"}), flush=True)
 L.close()
