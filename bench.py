@@ -12,6 +12,11 @@ value = nodes/s.
 
 N = 1: ogbn-products-shaped (BASELINE configs[1]): N = 2,449,029, F = 100, K = 3 (H = 4),
 B = 8192, HBM-resident fp32 hop features (synthetic, §8(d) generator G), bf16 batches.
+Secondary keys at N = 1 (each measured after the headline, in its own subprocess where
+noted): per_batch_call, gather_only, consumer_fused_linear (§8(f)-1), e2e (host-resident
+store over PCIe), double_buffer (§8(a) A6, subprocess), next_rows (§8(f)-2 propagation,
+§8(f)-3 storage tier, papers100M compact store; subprocesses), cpu_baseline (the oracle).
+
 N > 1 (torchrun): ogbn-papers100M-shaped (configs[2]): N = 111,059,956, F = 128, K = 3,
 B = 8192 per rank, chunk reshuffle c = 8192, nodes sharded round-robin over the ranks,
 rows read from the owners' HBM by NVLink peer loads (CUDA IPC).
@@ -337,6 +342,8 @@ def run_ours(args):
         result["e2e"] = e2e_host_store(pp, torch, cfg, args)
     if W == 1 and name == "products" and not args.skip_double_buffer:
         result["double_buffer"] = double_buffer_secondary()
+    if W == 1 and name == "products" and not args.skip_next_rows:
+        result["next_rows"] = next_rows_secondary()
     if rank == 0 and W == 1 and not args.skip_cpu:
         nthreads = os.cpu_count() or 1
         s, inf = oracle_epoch_sample(cfg, 32, nthreads)
@@ -399,6 +406,44 @@ def consumer_fused_linear(pp, torch, cfg, args, D=512, k=8, reps=5):
             "tflops": 2.0 * N * H * F * D / ms / 1e9,
             "note": "fused gather + cast + per-hop linear (tcgen05, TMEM accumulators); "
                     "unfused loader + cuBLAS reference: profiles/r1e_bench_fused_linear.jsonl"}
+
+
+def _script_lines(script, env_extra, timeout=600, args=()):
+    """Run a scripts/ measurement in a subprocess (own CUDA context); its JSON lines, or an error."""
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", script), *args], env=env, capture_output=True,
+                       text=True, timeout=timeout)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    if not lines:
+        raise RuntimeError((r.stderr or "no output")[-300:])
+    return lines
+
+
+def next_rows_secondary():
+    """The §8(f) rows measured by their scripts: GPU propagation (Eq. (2), products-sized graph),
+    the storage tier (hop files, chunk reshuffling) and the paper's papers100M setup (compact
+    store of the labelled nodes)."""
+    out = {}
+    try:
+        prop = _script_lines("bench_propagate.py", {})
+        out["propagation"] = {"ms_per_hop": prop[0]["ms_per_hop"], "frac_hbm": prop[0]["frac_hbm"],
+                              "into_store_ms_per_hop": prop[-1]["ms_per_hop"], "nnz": prop[0]["nnz"],
+                              "note": "bit-identical to the CPU oracle (tests/test_gpu_propagate*.py)"}
+    except Exception as e:
+        out["propagation"] = {"error": repr(e)[:300]}
+    try:
+        st = _script_lines("bench_storage.py", {"PP_STORAGE_EPOCHS": "1"})[-1]
+        out["storage_tier"] = {k: st[k] for k in ("chunk", "storage_mode", "nodes_per_s", "storage_GBs",
+                                                  "seq_read_GBs_measured", "frac_of_seq_read", "sampled_step_bit_exact")}
+    except Exception as e:
+        out["storage_tier"] = {"error": repr(e)[:300]}
+    try:
+        lab = _script_lines("bench_configs.py", {}, args=("papers100M-labelled",))
+        out["papers100M_labelled"] = [{k: d[k] for k in ("config", "N", "N_total", "ms_per_epoch", "nodes_per_s", "frac")}
+                                      for d in lab]
+    except Exception as e:
+        out["papers100M_labelled"] = {"error": repr(e)[:300]}
+    return out
 
 
 def double_buffer_secondary():
@@ -478,6 +523,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-consumer", action="store_true", help="skip the §8(f)-1 fused-linear measurement")
     ap.add_argument("--skip-double-buffer", action="store_true", help="skip the §8(a) A6 double-buffer measurement")
+    ap.add_argument("--skip-next-rows", action="store_true",
+                    help="skip the §8(f) propagation / storage-tier / compact-store measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
