@@ -71,7 +71,8 @@ steps = L.query()["steps_per_epoch"]
 bufs = [torch.empty((B, H, F), dtype=torch.bfloat16, device=dev) for _ in range(2)]
 labs = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(2)]
 cons = torch.cuda.Stream()
-loader_stream = torch.cuda.Stream()
+_prio = {"high": -5, "low": 0, "normal": 0}[os.environ.get("DB_LOADER_PRIO", "normal")]  # torch clamps to range
+loader_stream = torch.cuda.Stream(priority=_prio) if os.environ.get("DB_LOADER_PRIO") == "high" else torch.cuda.Stream()
 if GRAPH:  # one graph per (batch buffer, label buffer) pair; the ragged last batch runs eagerly
     ylong = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(2)]
     with torch.cuda.stream(cons):
@@ -167,7 +168,8 @@ for name, fn in (("loader", epoch_loader), (f"loader_{CTAS}ctas", lambda e: epoc
                  ("compute", epoch_compute), ("serial", epoch_serial), ("double", epoch_double),
                  (f"double_{CTAS}ctas", lambda e: epoch_double(e, CTAS))):
     res[name] = timeit(fn)
-    print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "graph": GRAPH, "mode": name, "ms_per_epoch": res[name],
+    print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "graph": GRAPH, "prio": os.environ.get("DB_LOADER_PRIO", "normal"),
+                      "gather": os.environ.get("PPLOAD_GATHER", "auto"), "mode": name, "ms_per_epoch": res[name],
                       "nodes_per_s": N / res[name] * 1e3}), flush=True)
 best = min(res["double"], res[f"double_{CTAS}ctas"])
 print(json.dumps({"placement": PLACEMENT, "chunk": CHUNK, "graph": GRAPH, "double_buffer_speedup": res["serial"] / best,
