@@ -174,12 +174,31 @@ __global__ void __launch_bounds__(256) k_bucket_rank(uint64_t seed, const uint32
                                                      uint32_t* __restrict__ pi) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t bucket = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; bucket < nb; bucket += nwarps) {
-  const uint32_t beg = offsets[bucket];
-  const uint32_t n = offsets[bucket + 1] - beg;
+  // Software pipeline over this warp's buckets (several per warp when the grid is capped, as
+  // for the prefetched permutation): the offsets of the bucket after next and the unit ids of
+  // the next bucket are loaded while the current one is ranked.
+  const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  auto load_range = [&](uint32_t b, uint32_t& beg_, uint32_t& n_) {
+    beg_ = 0;
+    n_ = 0;
+    if (b < nb) {
+      beg_ = offsets[b];
+      n_ = offsets[b + 1] - beg_;
+    }
+  };
+  uint32_t beg_cur, n_cur, beg_nxt, n_nxt;
+  load_range(first, beg_cur, n_cur);
+  load_range(first + nwarps, beg_nxt, n_nxt);
+  uint32_t ui_cur = (lane < static_cast<int>(n_cur) && n_cur <= 32) ? tmp[beg_cur + lane] : 0xffffffffu;
+  for (uint32_t bucket = first; bucket < nb; bucket += nwarps) {
+  const uint32_t beg = beg_cur, n = n_cur, ui_pre = ui_cur;
+  ui_cur = (lane < static_cast<int>(n_nxt) && n_nxt <= 32) ? tmp[beg_nxt + lane] : 0xffffffffu;
+  beg_cur = beg_nxt;
+  n_cur = n_nxt;
+  load_range(bucket + 2 * nwarps, beg_nxt, n_nxt);
   if (n <= 32) {
     const bool vi = lane < static_cast<int>(n);
-    const uint32_t ui = vi ? tmp[beg + lane] : 0xffffffffu;
+    const uint32_t ui = ui_pre;
     const uint64_t ki = vi ? unit_sort_key(seed, ui) : ~0ull;
     const uint32_t k32 = static_cast<uint32_t>((ki << bits) >> 32) & k32_mask;  // bits below the bucket prefix
     uint32_t rank = 0, eq = 0;
