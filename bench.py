@@ -425,20 +425,20 @@ def next_rows_secondary():
     store of the labelled nodes)."""
     out = {}
     try:
-        prop = _script_lines("bench_propagate.py", {})
+        prop = _script_lines("bench_propagate.py", {}, timeout=240)
         out["propagation"] = {"ms_per_hop": prop[0]["ms_per_hop"], "frac_hbm": prop[0]["frac_hbm"],
                               "into_store_ms_per_hop": prop[-1]["ms_per_hop"], "nnz": prop[0]["nnz"],
                               "note": "bit-identical to the CPU oracle (tests/test_gpu_propagate*.py)"}
     except Exception as e:
         out["propagation"] = {"error": repr(e)[:300]}
     try:
-        st = _script_lines("bench_storage.py", {"PP_STORAGE_EPOCHS": "1"})[-1]
+        st = _script_lines("bench_storage.py", {"PP_STORAGE_EPOCHS": "1"}, timeout=300)[-1]
         out["storage_tier"] = {k: st[k] for k in ("chunk", "storage_mode", "nodes_per_s", "storage_GBs",
                                                   "seq_read_GBs_measured", "frac_of_seq_read", "sampled_step_bit_exact")}
     except Exception as e:
         out["storage_tier"] = {"error": repr(e)[:300]}
     try:
-        lab = _script_lines("bench_configs.py", {}, args=("papers100M-labelled",))
+        lab = _script_lines("bench_configs.py", {}, timeout=240, args=("papers100M-labelled",))
         out["papers100M_labelled"] = [{k: d[k] for k in ("config", "N", "N_total", "ms_per_epoch", "nodes_per_s", "frac")}
                                       for d in lab]
     except Exception as e:
@@ -453,7 +453,7 @@ def double_buffer_secondary():
     env = dict(os.environ, DB_GRAPH="1", DB_PLACEMENT="host", DB_CHUNK="1", DB_CTAS="8", DB_EPOCHS="2")
     try:
         r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "bench_double_buffer.py")], env=env,
-                           capture_output=True, text=True, timeout=600)
+                           capture_output=True, text=True, timeout=300)
         lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
         modes = {d["mode"]: d["ms_per_epoch"] for d in lines if "mode" in d}
         summ = [d for d in lines if "double_buffer_speedup" in d]
