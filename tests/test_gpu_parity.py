@@ -637,3 +637,28 @@ def test_epoch_iterator_double_buffer(pp, tiny, depth, chunk):
             assert n[t] == want.shape[0]
             assert np.array_equal(got[t, :n[t]].cpu().view(torch.int16).numpy().view(np.uint16), want), t
             assert np.array_equal(gl[t, :n[t]].cpu().numpy(), wl) and np.array_equal(gv[t, :n[t]].cpu().numpy(), wn)
+
+
+@pytest.mark.parametrize("gather", ["ldg", "tma"])
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_grid_limit_bit_exact(pp, tiny, monkeypatch, gather, ctas):
+    # pp_set_grid_limit: a 1- or 3-CTA persistent grid walks every tile of every step in a launch
+    monkeypatch.setenv("PPLOAD_GATHER", gather)
+    hops, bits = tiny
+    H, N, F = hops.shape
+    B = 256
+    with pp.Loader(data=hops, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=N * F, row_stride=F, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.set_grid_limit(ctas)
+        L.epoch_permute(31, 4)
+        order = oracle.epoch_order(31, N, 4)
+        steps = oracle.num_steps(N, B)
+        ring = torch.empty((steps, B, H, F), dtype=torch.bfloat16, device="cuda")
+        rows = L.next_batches(steps, ring, B * H * F * 2)
+        torch.cuda.synchronize()
+        assert len(rows) == steps
+        for t, nr in enumerate(rows):
+            want, _, _ = oracle.batch(bits, oracle.F32, N * F, F, H, F, order, B, 1, t, 0, oracle.BF16)
+            assert np.array_equal(ring[t, :nr].cpu().view(torch.int16).numpy().view(np.uint16), want), t
+        with pytest.raises(pp.PPError):
+            L.set_grid_limit(-1)
