@@ -336,6 +336,39 @@ def run_ours(args):
     L.close()
     torch.cuda.empty_cache()
 
+    if W > 1 and not args.skip_weak:
+        # Weak-scaling companion of the N = 1 headline: a products-shaped shard per rank
+        # (N_total = 2,449,029 x W), one global permutation, (W-1)/W of every batch read from
+        # peers -- the per-GPU work of the single-GPU line, so the two compare directly.
+        N = CONFIGS["products"]["N"] * W
+        H, F, B, chunk = CONFIGS["products"]["H"], CONFIGS["products"]["F"], CONFIGS["products"]["B"], 1
+        L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
+                      device=local, world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
+        L.fill_synthetic(DATA_SEED)
+        hs = [None] * W
+        dist.all_gather_object(hs, pp.pp_export_store(L.h))
+        pp.pp_import_peer_stores(L.h, b"".join(hs))
+        L.set_stream(stream)
+        info = L.query()
+        steps = info["steps_per_epoch"]
+        rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
+        slot_bytes = B * H * F * 2
+        nslots = min(steps, max(args.per_call, int(4e9 // slot_bytes)))
+        ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
+        slots = list(ring.unbind(0))
+        my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
+        mw = timed(k, args.steps)
+        result["weak_products"] = {
+            "value": N * args.steps / (mw["total_ms"] / 1e3), "unit": UNIT, "num_nodes": N,
+            "ms_per_step": mw["total_ms"] / args.steps, "per_gpu_nodes_per_s": N * args.steps / (mw["total_ms"] / 1e3) / W,
+            "exchange_cast": bool(info["exchange_cast"]),
+            "note": "products-shaped shard per rank, global permutation, peer reads; same per-GPU work as N = 1"}
+        del ring, slots
+        torch.cuda.synchronize()
+        dist.barrier()
+        L.close()
+        torch.cuda.empty_cache()
+
     if W == 1 and name == "products" and not args.skip_consumer:
         result["consumer_fused_linear"] = consumer_fused_linear(pp, torch, cfg, args)
     if W == 1 and not args.skip_e2e:
@@ -523,6 +556,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-consumer", action="store_true", help="skip the §8(f)-1 fused-linear measurement")
     ap.add_argument("--skip-double-buffer", action="store_true", help="skip the §8(a) A6 double-buffer measurement")
+    ap.add_argument("--skip-weak", action="store_true", help="N > 1: skip the products-shaped weak-scaling line")
     ap.add_argument("--skip-next-rows", action="store_true",
                     help="skip the §8(f) propagation / storage-tier / compact-store measurements")
     args = ap.parse_args()
