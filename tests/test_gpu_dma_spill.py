@@ -126,3 +126,20 @@ def test_dma_and_kernel_paths_agree_with_seek(pp, monkeypatch):
     assert len(outs["dma"]) == len(outs["kernel"]) == oracle.num_steps(N, B) - 5
     for a, b in zip(outs["dma"], outs["kernel"]):
         assert np.array_equal(a, b)
+
+
+def test_epoch_iterator_over_dma_path(pp):
+    # the double-buffered iterator (per-buffer events) with host rows moved by the copy engines
+    H, N, F, B, chunk = 4, 3000, 32, 128, 128
+    X, hs, rs = hop_tensor(95, H, N, F)
+    L = pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                  batch_size=B, out_dtype=pp.PP_BF16, hbm_budget_bytes=-1)
+    order = oracle.epoch_order(6, N, chunk)
+    got = [(x.clone(), v.clone()) for x, _, v in L.epoch(6, chunk, depth=2, nodes=True)]
+    torch.cuda.synchronize()
+    assert len(got) == oracle.num_steps(N, B)
+    for t, (x, v) in enumerate(got):
+        want, _, wn = oracle.batch(X.view(np.uint32), oracle.F32, hs, rs, H, F, order, B, 1, t, 0, oracle.BF16)
+        assert np.array_equal(bits_of(x, oracle.BF16), want), t
+        assert np.array_equal(v.cpu().numpy(), wn), t
+    L.close()

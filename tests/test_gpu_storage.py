@@ -190,3 +190,23 @@ def test_invalid_file_loaders(pp, tmp_path):
         assert ei.value.status == pp.PP_ERR_INVALID
     L.close()
 
+
+
+def test_epoch_iterator_over_files(pp, tmp_path):
+    # the double-buffered iterator (per-buffer events) on the storage tier
+    H, N, F, B, chunk = 3, 2500, 32, 128, 64
+    hops = np.random.default_rng(55).standard_normal((H, N, F)).astype(np.float32)
+    L = pp.Loader(files=write_hops(tmp_path, hops), num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32,
+                  batch_size=B, out_dtype=pp.PP_BF16)
+    order = oracle.epoch_order(5, N, chunk)
+    got = []
+    for x, _, v in L.epoch(5, chunk, depth=3, nodes=True):
+        torch.cuda._sleep(10000)
+        got.append((x.clone(), v.clone()))
+    torch.cuda.synchronize()
+    assert len(got) == oracle.num_steps(N, B)
+    for t, (x, v) in enumerate(got):
+        want, _, wn = oracle.batch(hops.view(np.uint32), oracle.F32, N * F, F, H, F, order, B, 1, t, 0, oracle.BF16)
+        assert np.array_equal(bits_of(x, oracle.BF16), want), t
+        assert np.array_equal(v.cpu().numpy(), wn), t
+    L.close()
