@@ -102,7 +102,7 @@ struct pp_loader {
   // CTA cap for the prefetched permutation (PPLOAD_PREFETCH_CTAS; 0 = full grid).
   // Measured on products (profiles/r1j_exp_prefetch.jsonl): full grid 1.002 ms/epoch,
   // 148-296 CTAs 0.972 ms, 64 CTAs 1.11-1.15 ms (the sort then outlasts the epoch).
-  int prefetch_ctas = 296;
+  int prefetch_ctas = 148;  // r1zz: 148 >= 296 > 444 once k_bucket_rank pipelines its loads
   int max_ctas = 0;  // pp_set_grid_limit: cap on the gather grid (0 = the full persistent grid)
   // previous op on the loader stream (programmatic dependent launch is only used
   // between consecutive launches of the same kind within one epoch)
