@@ -53,27 +53,66 @@ def log(*a):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML every ~2 ms (the timed
+    region of a products run is only tens of ms), nvidia-smi every 100 ms if NVML is unavailable."""
 
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvml"
+        self._nvml = None
+        try:  # initialise NVML before the timed region starts (nvmlInit takes tens of ms)
+            import pynvml
 
-    def _run(self):
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(max(0, index))
+            self._nvml = (pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+
+    def _run_nvml(self):
+        if self._nvml is None:
+            raise RuntimeError("NVML unavailable")
+        pynvml, h, mx = self._nvml
+        bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        try:
+            while True:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), {n for n, bit in zip(self.NAMES, bits) if r & bit}))
+                if self._stop.wait(0.002):
+                    break
+        finally:
+            pynvml.nvmlShutdown()
+
+    def _run_smi(self):
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
+                    r = [x.strip() for x in line.split(",")]
+                    if r[0].replace(".", "").isdigit():
+                        self.rows.append((float(r[0]), float(r[1]),
+                                          {self.NAMES[i] for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"}))
             except Exception:
                 pass
             self._stop.wait(0.1)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            if not self._stop.is_set():
+                self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -87,12 +126,9 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows),
+                "source": self.source}
 
 
 def peaks():
@@ -251,8 +287,8 @@ def run_ours(args):
         if dist:
             dist.barrier()
         evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(nsteps)]
-        clk = ClockSampler(sampler_index if sampler_index is not None else -1)
-        if sampler_index is not None:
+        clk = ClockSampler(sampler_index) if sampler_index is not None else None
+        if clk is not None:
             clk.__enter__()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -264,7 +300,7 @@ def run_ours(args):
                 evs[i][2].record(stream)
             end.record(stream)
         torch.cuda.synchronize()
-        if sampler_index is not None:
+        if clk is not None:
             clk.__exit__(None, None, None)
         if dist:
             dist.barrier()
@@ -282,7 +318,7 @@ def run_ours(args):
         bytes_per_launch = my_rows * (rec_in + rec_out + 4) / launches
         return {"total_ms": t[0], "gather_ms": t[1], "perm_ms": t[2], "per_launch_ms": per_launch_ms,
                 "bytes_per_launch": bytes_per_launch, "achieved": bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
-                "launches": launches, "clocks": clk.summary() if sampler_index is not None else None}
+                "launches": launches, "clocks": clk.summary() if clk is not None else None}
 
     k = max(1, args.per_call)
     m = timed(k, args.steps, sampler_index=local)
