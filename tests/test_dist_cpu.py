@@ -35,7 +35,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_handle_exchange_and_arg_check_gloo(world):
     import sys
 
