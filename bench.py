@@ -208,6 +208,35 @@ def config_dict(name, cfg, W, l2):
 
 
 # --------------------------------------------------------------------------- GPU arm
+def epoch_loop(L, seed, next_seed, chunk, steps, slots, slot_bytes, k, stream, node_slots=None, ev_mid=None):
+    """One timed step: pp_epoch_permute(seed) (switches to the prefetched order when the previous
+    epoch prefetched it), pp_epoch_prefetch(next_seed) on the side stream, then every batch of the
+    epoch, k per pp_next_batches launch (k = 1: pp_next_batch), into consecutive slots of the ring
+    (a call never wraps it).  tests/test_gpu_timed_path.py runs this exact loop against the oracle."""
+    L.epoch_permute(seed, chunk, stream)
+    if next_seed is not None:
+        L.epoch_prefetch(next_seed, chunk)  # next epoch's order overlaps this epoch's batches
+    if ev_mid is not None:
+        ev_mid.record(stream)
+    nslots = len(slots)
+    done = 0
+    while done < steps:
+        s0 = done % nslots
+        nodes = None if node_slots is None else node_slots[s0]
+        if k == 1:
+            L.next_batch(slots[s0], None, nodes, stream)
+            done += 1
+        else:
+            n = min(k, steps - done, nslots - s0)
+            done += len(L.next_batches(n, slots[s0], slot_bytes, None, nodes, stream))
+
+
+def ring_slots(steps, per_call, slot_bytes):
+    """Output ring of the timed loop: one slot per step of the epoch, capped at 4 GB (>= 1 GB >> L2,
+    so the outputs go to DRAM)."""
+    return min(steps, max(per_call, int(4e9 // slot_bytes)))
+
+
 def run_ours(args):
     import torch
 
@@ -251,9 +280,8 @@ def run_ours(args):
     steps = info["steps_per_epoch"]
     rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
 
-    # output ring: one slot per step of the epoch, capped at 4 GB (>= 1 GB >> L2: outputs go to DRAM)
     slot_bytes = B * H * F * 2
-    nslots = min(steps, max(args.per_call, int(4e9 // slot_bytes)))
+    nslots = ring_slots(steps, args.per_call, slot_bytes)
     ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
     slots = list(ring.unbind(0))  # slot views made once, not per call (torch indexing costs ~1 us)
     # rows this rank assembles per epoch (for the algorithmic bytes)
@@ -265,20 +293,8 @@ def run_ours(args):
 
     def timed(k, nsteps, sampler_index=None):
         def epoch(e, ev_mid=None):
-            L.epoch_permute(SEED0 + e, chunk, stream)
-            if args.prefetch:
-                L.epoch_prefetch(SEED0 + e + 1, chunk)  # next epoch's order overlaps this epoch's batches
-            if ev_mid is not None:
-                ev_mid.record(stream)
-            done = 0
-            while done < steps:
-                s0 = done % nslots
-                if k == 1:
-                    L.next_batch(slots[s0], None, None, stream)
-                    done += 1
-                else:
-                    n = min(k, steps - done, nslots - s0)
-                    done += len(L.next_batches(n, slots[s0], slot_bytes, None, None, stream))
+            epoch_loop(L, SEED0 + e, SEED0 + e + 1 if args.prefetch else None, chunk, steps, slots, slot_bytes, k,
+                       stream, ev_mid=ev_mid)
 
         with torch.cuda.stream(stream):
             for e in range(args.warmup):

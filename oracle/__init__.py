@@ -52,6 +52,8 @@ def lib():
                 "ppo_philox4x32_10": (None, [P, P, P]),
                 "ppo_unit_key": (u64, [u64, u64]),
                 "ppo_unit_keys": (None, [u64, i64, P]),
+                "ppo_philox_batch": (None, [P, P, i64, P]),
+                "ppo_unit_key_batch": (None, [u64, P, i64, P]),
                 "ppo_unit_permutation": (ctypes.c_int, [u64, i64, P]),
                 "ppo_epoch_order": (ctypes.c_int, [u64, i64, i64, P]),
                 "ppo_apply_node_set": (None, [P, i64, P]),
@@ -92,6 +94,23 @@ def philox(ctr, key) -> np.ndarray:
     k = np.ascontiguousarray(key, dtype=np.uint32)
     out = np.zeros(4, dtype=np.uint32)
     lib().ppo_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def philox_batch(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
+    """O4 over many inputs: ctr [n, 4] u32, key [n, 2] u32 -> [n, 4] u32."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros((c.shape[0], 4), dtype=np.uint32)
+    lib().ppo_philox_batch(_p(c), _p(k), c.shape[0], _p(out))
+    return out
+
+
+def unit_key_at(seed: int, units) -> np.ndarray:
+    """O5: sort keys of arbitrary (64-bit) unit ids."""
+    u = np.ascontiguousarray(units, dtype=np.uint64)
+    out = np.zeros(u.shape[0], dtype=np.uint64)
+    lib().ppo_unit_key_batch(seed, _p(u), u.shape[0], _p(out))
     return out
 
 

@@ -15,7 +15,11 @@
  * paper adopted where the paper is silent are listed in DESIGN.md §3).
  *
  * Pins (what this oracle is checked against, see tests/test_oracle_*.py):
- *   philox        -- Random123 known-answer vectors (golden file).
+ *   philox        -- Random123 known-answer vectors (golden file) and, on a
+ *                    B200, cuRAND's curand_Philox4x32_10 over 10^6 random
+ *                    (ctr, key) pairs (tests/test_gpu_curand_pins.py).
+ *   unit keys     -- the O5 word layout against cuRAND for seeds with both
+ *                    halves nonzero and u >= 2^32 (same test file).
  *   unit keys /
  *   permutation   -- bijection, chi^2 uniformity over the 24 perms of n=4,
  *                    CR(c=1) == RR, chunk contiguity, numpy lexsort brute force.
@@ -25,7 +29,8 @@
  *                    plus hand-derived special values.
  *   propagation   -- dense fp64 matrix power (numpy), ring/complete/edgeless
  *                    closed forms, sqrt(d~) fixed point, SPEC worked values.
- *   generators    -- range/normality properties + golden first values.
+ *   generators    -- range/normality properties; the generator words against
+ *                    cuRAND's Philox on the O11 counter layout (same test file).
  * Nothing here is "parity unpinned".
  */
 #include <math.h>
@@ -81,6 +86,15 @@ uint64_t ppo_unit_key(uint64_t seed, uint64_t u) {
 
 void ppo_unit_keys(uint64_t seed, int64_t U, uint64_t* keys) {
   for (int64_t u = 0; u < U; ++u) keys[u] = ppo_unit_key(seed, (uint64_t)u);
+}
+
+/* Batch forms for the pin tests (loops over the functions above, no arithmetic of their own). */
+void ppo_philox_batch(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out) {
+  for (int64_t i = 0; i < n; ++i) ppo_philox4x32_10(ctr + 4 * i, key + 2 * i, out + 4 * i);
+}
+
+void ppo_unit_key_batch(uint64_t seed, const uint64_t* u, int64_t n, uint64_t* keys) {
+  for (int64_t i = 0; i < n; ++i) keys[i] = ppo_unit_key(seed, u[i]);
 }
 
 typedef struct {

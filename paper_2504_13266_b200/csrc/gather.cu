@@ -238,8 +238,15 @@ __global__ void __launch_bounds__(kGatherThreads, kMinBlocksPerSM)
     for (uint32_t e = threadIdx.x; e < nel; e += kGatherThreads) {
       const uint32_t r = fast_div(e, HF_M);
       const uint32_t i = e - r * HF;
-      const uint8_t* src = s_src[buf][r] + static_cast<int64_t>(i) * s_in;
+      const uint8_t* row = s_src[buf][r];
       uint8_t* dst = out_tile + static_cast<int64_t>(r) * row_out_bytes + static_cast<int64_t>(i) * s_out;
+      if (SHARDED && (reinterpret_cast<uintptr_t>(row) & 1u)) {
+        // a peer's exchange copy (bit 0 tags it, see resolve_rows): elements already in the batch dtype
+        *reinterpret_cast<uint16_t*>(dst) =
+            __ldg(reinterpret_cast<const unsigned short*>(row - 1 + static_cast<int64_t>(i) * 2));
+        continue;
+      }
+      const uint8_t* src = row + static_cast<int64_t>(i) * s_in;
       if (s_in == 4) {
         const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
         if (a.out_dtype == kBF16) {

@@ -184,8 +184,8 @@ bool file_tier_set_epoch(FileTier* T, uint64_t epoch, const uint32_t* order, con
                          int32_t W, int32_t rank, int64_t steps, std::string* err);
 // Assemble `step` into out on st (waits for its reads; keeps the next steps staging).
 cudaError_t file_tier_step(FileTier* T, int64_t step, int32_t in_dtype, int32_t out_dtype, const int32_t* labels,
-                           uint8_t* out, int32_t* out_labels, int64_t* out_nodes, cudaStream_t st, int32_t* rows,
-                           std::string* err);
+                           uint8_t* out, int32_t* out_labels, int64_t* out_nodes, bool out_vec, cudaStream_t st,
+                           int32_t* rows, std::string* err);
 
 // order (u32 positions) -> global node ids (int64), for pp_get_order.
 cudaError_t launch_order_to_nodes(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t* dst,

@@ -108,6 +108,19 @@ struct pp_loader {
   // between consecutive launches of the same kind within one epoch)
   enum { kLastNone = 0, kLastGather = 1, kLastLinear = 2 };
   int last_kernel = kLastNone;
+  // Byte ranges written by the launches of the current programmatic-dependent-launch chain (hulls):
+  // chained launches may run concurrently, so a launch whose outputs overlap them is not chained.
+  struct Span {
+    uintptr_t lo = 0, hi = 0;
+    bool overlaps(const Span& o) const { return lo < hi && o.lo < o.hi && lo < o.hi && o.lo < hi; }
+    void join(const Span& o) {
+      if (o.lo >= o.hi) return;
+      if (lo >= hi) { *this = o; return; }
+      lo = std::min(lo, o.lo);
+      hi = std::max(hi, o.hi);
+    }
+  };
+  Span chain[3];  // out (or Z), labels, node ids
 
   ShardView shards[kMaxWorld]{};
   bool linked = false;
@@ -248,6 +261,8 @@ int prefetch_priority() {
   if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
   return least;
 }
+
+bool fast_div_ok(int64_t d) { return d > 0 && static_cast<uint64_t>(128) * d * d < (uint64_t(1) << 40); }
 
 pp_status validate(const pp_loader_desc* d) {
   if (!d) return fail(PP_ERR_INVALID, "desc is NULL");
@@ -421,6 +436,13 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   L->rec_stride = (L->rec_in + 15) / 16 * 16;
   L->rec_out = static_cast<int64_t>(L->HF) * elem_bytes(L->out_dtype);
   L->vector_path = gather_vector_ok(L->HF, L->in_dtype, L->out_dtype, L->rec_stride);
+  // the gather kernels divide slot indices by a 2^40 reciprocal: tile (<= 128 rows) x slots per row
+  // x divisor must stay below 2^40 (vector path: vpr = rec_out / 16 slots; scalar: H*F elements)
+  if (!fast_div_ok(L->vector_path ? L->rec_out / 16 : L->HF)) {
+    release(L);
+    return fail(PP_ERR_INVALID, "record of H*F = %d elements too large for the %s gather path", L->HF,
+                L->vector_path ? "vector" : "scalar");
+  }
 
   auto bail = [&](pp_status s) {
     release(L);
@@ -489,6 +511,10 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (e == cudaSuccess && L->n_spill > 0) e = copy_in(L, desc->hops, L->n_hbm, L->n_spill, L->h_spill);
     if (e != cudaSuccess) return bail(fail(PP_ERR_CUDA, "store upload failed: %s", cudaGetErrorString(e)));
   }
+  // The uploads above run on the legacy stream (cudaMemcpy2D may return before a device-source or
+  // staged copy lands); the exchange copy below reads d_store on the non-blocking loader stream.
+  if (desc->hops.data && !files && !L->borrowed && cudaDeviceSynchronize() != cudaSuccess)
+    return bail(fail(PP_ERR_CUDA, "store upload sync failed"));
   // ---- labels, order, sort scratch
   if (desc->labels) {
     L->has_labels = true;
@@ -784,7 +810,8 @@ struct StepOut {
   int32_t* labels;
   int64_t* nodes;
   int32_t* rows;
-  bool vec;  // 16-byte aligned slots: the vector kernels apply
+  bool vec;      // 16-byte aligned slots and a vector-path record: the vector kernels apply
+  bool aligned;  // 16-byte aligned slots (out and its pitch)
 };
 
 // Storage tier: each step's rows are read from the hop files, then assembled on the GPU.
@@ -793,7 +820,7 @@ static pp_status enqueue_file_steps(pp_loader* L, int64_t nsteps, const StepOut&
     std::string err;
     cudaError_t e = file_tier_step(L->files, L->cursor + i, L->in_dtype, L->out_dtype, L->d_labels, o.out + i * o.stride,
                                    o.labels ? o.labels + i * L->B : nullptr, o.nodes ? o.nodes + i * L->B : nullptr,
-                                   L->stream, &o.rows[i], &err);
+                                   o.aligned, L->stream, &o.rows[i], &err);
     if (e == cudaErrorUnknown) {
       L->poisoned = true;
       return fail(PP_ERR_CUDA, "storage tier: %s", err.c_str());
@@ -835,6 +862,19 @@ static pp_status enqueue_dma_steps(pp_loader* L, int64_t nsteps, const StepOut& 
   return PP_OK;
 }
 
+// Whether the next launch of `kind` may be chained to the previous one by programmatic dependent
+// launch (only after a launch of the same kind, and only if its output spans do not overlap any
+// span written by the chain so far); updates the chain's hulls.
+static bool chain_pdl(pp_loader* L, int kind, const pp_loader::Span (&spans)[3]) {
+  bool pdl = L->pdl && L->last_kernel == kind;
+  for (int i = 0; i < 3 && pdl; ++i) pdl = !L->chain[i].overlaps(spans[i]);
+  for (int i = 0; i < 3; ++i) {
+    if (!pdl) L->chain[i] = pp_loader::Span{};
+    L->chain[i].join(spans[i]);
+  }
+  return pdl;
+}
+
 // HBM / zero-copy host / peer rows: the gather kernels, all nsteps in one launch.
 static pp_status enqueue_gather_steps(pp_loader* L, int64_t nsteps, const StepOut& o, bool pdl_ok) {
   GatherArgs a{};
@@ -871,8 +911,18 @@ static pp_status enqueue_gather_steps(pp_loader* L, int64_t nsteps, const StepOu
   if (o.vec && L->tma_ok && (L->gather_mode == 2 || (L->gather_mode == 0 && remote))) path = kPathTma;
   // Programmatic dependent launch only right after another gather of this epoch: batches of
   // one epoch are independent, and the first gather after a permute or an event wait is
-  // fully serialised, so every gather sees a complete order.
-  PPL_CUDA(L, launch_gather(a, path, L->pdl && L->last_kernel == pp_loader::kLastGather, L->grid_per_sm, L->stream));
+  // fully serialised, so every gather sees a complete order.  A launch that rewrites memory an
+  // earlier launch of the chain writes (a reused slot) is serialised too (chain_pdl).
+  const auto span = [](const void* p, int64_t bytes) {
+    pp_loader::Span sp;
+    sp.lo = reinterpret_cast<uintptr_t>(p);
+    sp.hi = p ? sp.lo + static_cast<uintptr_t>(bytes) : sp.lo;
+    return sp;
+  };
+  const pp_loader::Span spans[3] = {span(o.out, (nsteps - 1) * o.stride + L->B * L->rec_out),
+                                    span(o.labels, nsteps * L->B * 4), span(o.nodes, nsteps * L->B * 8)};
+  const bool pdl = chain_pdl(L, pp_loader::kLastGather, spans);
+  PPL_CUDA(L, launch_gather(a, path, pdl, L->grid_per_sm, L->stream));
   // the next gather may overlap this one unless an event record follows it (pdl_ok false)
   L->last_kernel = pdl_ok ? pp_loader::kLastGather : pp_loader::kLastNone;
   for (int64_t i = 0; i < nsteps; ++i) {
@@ -900,6 +950,9 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   if (nsteps > 1 && out_stride < L->B * L->rec_out)
     return fail(PP_ERR_INVALID, "out_stride_bytes %lld < one batch (%lld)", (long long)out_stride,
                 (long long)(L->B * L->rec_out));
+  const bool aligned = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0);
+  if (!(L->vector_path && aligned) && !L->files && !L->dma_epoch && !fast_div_ok(L->HF))
+    return fail(PP_ERR_INVALID, "records of H*F = %d elements need a 16-byte aligned out / out_stride", L->HF);
   DevGuard g(L->dev);
   // ---- consumer -> loader (WAR on `out`)
   const bool handoff = !ho.events && ho.cons != L->stream;
@@ -913,8 +966,7 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
     L->last_kernel = pp_loader::kLastNone;
   }
   // ---- the steps
-  StepOut o{static_cast<uint8_t*>(out), out_stride, out_labels, out_nodes, rows,
-            L->vector_path && (reinterpret_cast<uintptr_t>(out) % 16 == 0) && (out_stride % 16 == 0)};
+  StepOut o{static_cast<uint8_t*>(out), out_stride, out_labels, out_nodes, rows, L->vector_path && aligned, aligned};
   const bool signals = handoff || (ho.events && ho.ready_ev);  // an event record follows the steps
   pp_status st = L->files ? enqueue_file_steps(L, nsteps, o)
                  : L->dma_epoch ? enqueue_dma_steps(L, nsteps, o)
@@ -1013,7 +1065,11 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
     PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, (24 * 14 + 4 * 1024) * 8, L->stream));
     a.ts = dbg_ts;
   }
-  PPL_CUDA(L, launch_gather_linear(a, L->pdl && !handoff && L->last_kernel == pp_loader::kLastLinear, L->stream));
+  pp_loader::Span zspans[3];
+  zspans[0].lo = reinterpret_cast<uintptr_t>(Z);
+  zspans[0].hi = zspans[0].lo + static_cast<uintptr_t>((nsteps - 1) * z_stride_bytes + L->B * L->H * D * z_elem);
+  const bool pdl = !handoff && chain_pdl(L, pp_loader::kLastLinear, zspans);
+  PPL_CUDA(L, launch_gather_linear(a, pdl, L->stream));
   if (want_ts) {
     static uint64_t h[24 * 14 + 4 * 1024];
     PPL_CUDA(L, cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, L->stream));

@@ -402,6 +402,17 @@ FileTier* file_tier_open(const char* const* paths, int H, int64_t N_total, int F
       delete T;
       return nullptr;
     }
+    // Headerless raw [N_total][F] only: a file with the PPGF container header (magic, version,
+    // data offset, per-chunk padding) would be misread row by row, so it is refused.
+    char magic[4] = {0, 0, 0, 0};
+    const int fd_probe = open(paths[k], O_RDONLY);  // buffered: O_DIRECT reads need aligned buffers
+    const bool ppgf = fd_probe >= 0 && pread(fd_probe, magic, 4, 0) == 4 && !memcmp(magic, "PPGF", 4);
+    if (fd_probe >= 0) close(fd_probe);
+    if (ppgf) {
+      *err = std::string(paths[k]) + ": PPGF container files are not supported (raw [N_total][F] hop files only)";
+      delete T;
+      return nullptr;
+    }
   }
   if (!T->direct) {
     for (int k = 0; k < H; ++k) {  // all files the same way
@@ -459,8 +470,8 @@ bool file_tier_set_epoch(FileTier* T, uint64_t epoch, const uint32_t* order, con
 }
 
 cudaError_t file_tier_step(FileTier* T, int64_t step, int32_t in_dtype, int32_t out_dtype, const int32_t* labels,
-                           uint8_t* out, int32_t* out_labels, int64_t* out_nodes, cudaStream_t st, int32_t* rows,
-                           std::string* err) {
+                           uint8_t* out, int32_t* out_labels, int64_t* out_nodes, bool out_vec, cudaStream_t st,
+                           int32_t* rows, std::string* err) {
   const int64_t depth = static_cast<int64_t>(T->slots.size());
   if (!T->staged(step)) T->dispatch(step);
   for (int64_t d = step + 1; d < std::min(step + depth, T->steps); ++d)  // keep the window full
@@ -483,7 +494,8 @@ cudaError_t file_tier_step(FileTier* T, int64_t step, int32_t in_dtype, int32_t 
     if (e == cudaSuccess) e = cudaEventRecord(cur.ev_h2d, st);
     if (e != cudaSuccess) return e;
     cur.h2d_pending = true;
-    const bool vec = T->F % 4 == 0 && T->rb % 16 == 0;
+    // 4-element vectors need F % 4 == 0 and a 16-B aligned `out` / slot pitch (out_vec)
+    const bool vec = out_vec && T->F % 4 == 0 && T->rb % 16 == 0;
     const int64_t units = static_cast<int64_t>(cur.rows) * T->H * (vec ? T->F / 4 : T->F);
     const uint32_t grid = static_cast<uint32_t>(std::min<int64_t>((units + 255) / 256, 148 * 16));
     const int64_t* row_src = reinterpret_cast<const int64_t*>(cur.d);
