@@ -48,10 +48,13 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 5
+#define PP_ABI_VERSION 6
 
 /* Bytes of one rank's exported store handle (pp_export_store). */
-#define PP_IPC_HANDLE_BYTES 128
+#define PP_IPC_HANDLE_BYTES 256
+
+/* Bytes of an NCCL unique id (pp_nccl_unique_id, pp_loader_desc.nccl_unique_id). */
+#define PP_NCCL_ID_BYTES 128
 
 typedef struct pp_loader pp_loader; /* opaque handle */
 
@@ -60,7 +63,7 @@ typedef enum {
   PP_ERR_INVALID = 1,   /* bad argument; no side effects */
   PP_ERR_OOM = 2,       /* device or pinned-host allocation failed */
   PP_ERR_CUDA = 3,      /* CUDA runtime error; handle poisoned */
-  PP_ERR_NCCL = 4,      /* reserved for a collective transport; handle poisoned */
+  PP_ERR_NCCL = 4,      /* NCCL failure (PP_PEERS_NCCL); handle poisoned */
   PP_ERR_STATE = 5,     /* call out of order (e.g. next_batch before any permute) */
   PP_END_OF_EPOCH = 6   /* cursor exhausted; *rows = 0, nothing enqueued */
 } pp_status;
@@ -74,8 +77,14 @@ typedef enum {
   PP_PEERS_NONE = 0,     /* W == 1 */
   PP_PEERS_IPC = 1,      /* one process per GPU; handles exchanged with
                             pp_export_store / pp_import_peer_stores */
-  PP_PEERS_LOOPBACK = 2  /* W shards in ONE process on ONE device, linked with
+  PP_PEERS_LOOPBACK = 2, /* W shards in ONE process on ONE device, linked with
                             pp_link_loopback (tests the sharded path on 1 GPU) */
+  PP_PEERS_NCCL = 3      /* one process per GPU; every step's rows are exchanged by an
+                            NCCL all-to-all (ncclSend / ncclRecv):
+                            each owner packs the rows it holds for every rank (cast
+                            fused), the receiver unpacks them into batch order.  Needs
+                            desc.nccl_unique_id.  Also valid with W == 1 (a
+                            self-exchange through NCCL). */
 } pp_peers;
 
 /* The K+1 hop matrices X_0..X_K.
@@ -124,9 +133,13 @@ typedef struct {
   int32_t drop_last;        /* 0: keep the ragged last step; 1: drop it */
   int64_t hbm_budget_bytes; /* bytes of HBM for this rank's store; rows
                                beyond it spill to pinned mapped host memory.
-                               0 => (free HBM - 2 GiB reserve); < 0 => all
-                               rows in host memory (the paper's host
-                               placement).  W > 1 requires no spill.
+                               0 => (free HBM - 2 GiB reserve - this
+                               loader's own scratch); < 0 => all rows in host
+                               memory (the paper's host placement).  W > 1 with
+                               PP_PEERS_IPC: the spill is an anonymous
+                               shared-memory file (memfd) that the peers map
+                               and register too, so every
+                               rank reads another's spilled rows zero-copy.
                                Host-resident rows are read zero-copy by the
                                gather kernel; under chunk reshuffling
                                (chunk >= 64, PPLOAD_DMA_MIN_CHUNK) each step's
@@ -136,7 +149,8 @@ typedef struct {
                                (PPLOAD_SPILL_PATH=dma|kernel forces a path). */
   int32_t world_size;       /* W >= 1 */
   int32_t rank;             /* 0 <= r < W */
-  pp_peers peers;           /* PP_PEERS_NONE iff W == 1 (file loaders: always
+  pp_peers peers;           /* W == 1: PP_PEERS_NONE (or PP_PEERS_NCCL); W > 1:
+                               IPC, LOOPBACK or NCCL (file loaders: always
                                PP_PEERS_NONE, any W) */
   int32_t device;           /* CUDA device ordinal */
   int32_t store_set_only;   /* 1: the store holds only the node_set rows ("the input
@@ -157,6 +171,9 @@ typedef struct {
                                pp_propagate_store write into it.  Needs W == 1,
                                no store_set_only and the whole store in HBM,
                                else PP_ERR_INVALID.  0: copy (default). */
+  const void* nccl_unique_id; /* PP_PEERS_NCCL: PP_NCCL_ID_BYTES from pp_nccl_unique_id on one
+                               rank, broadcast by the caller (e.g. torch.distributed); NULL
+                               otherwise.  Read during pp_loader_create only. */
 } pp_loader_desc;
 
 /* Read-only facts about a loader (pp_loader_query). */
@@ -180,6 +197,16 @@ typedef struct {
                                peers read instead of the fp32 records (W > 1, see below) */
   int32_t storage_mode;     /* 0: no file tier; 1: file tier with O_DIRECT reads; 2: buffered reads */
   int64_t storage_bytes_read; /* bytes read from the hop files so far (aligned extents included) */
+  /* ABI 6 */
+  int64_t pdl_launches;     /* batch launches chained to the previous one by programmatic dependent
+                               launch so far (a launch rewriting a slot the chain writes is not) */
+  int32_t all_to_all;       /* 1: steps are exchanged by the all-to-all path (PP_PEERS_NCCL, or
+                               PP_PEERS_LOOPBACK with PPLOAD_EXCHANGE=a2a) */
+  int32_t spill_shared;     /* 1: the spill is a shared-memory file the peers map (PP_PEERS_IPC) */
+  int64_t hbm_store_bytes;  /* memory plan: HBM part of the store (0 if borrowed) */
+  int64_t hbm_exchange_bytes; /* exchange copy (cast rows for the peers) */
+  int64_t hbm_scratch_bytes;  /* order buffers, sort scratch, exchange buffers allocated so far */
+  int64_t host_spill_bytes;   /* pinned host spill */
 } pp_loader_info;
 
 /* Create a loader.  Copies the hop data into a library-owned, node-major store
@@ -200,8 +227,16 @@ pp_status pp_loader_destroy(pp_loader* L);
  * the cursor to step 0.  1 <= chunk <= N (chunk = 1: SGD-RR; chunk = c:
  * chunk reshuffling).  Runs on the loader stream after all work
  * enqueued on `stream` so far; later pp_next_batch calls are ordered after it.
- * Collective for W > 1: every rank passes the same (seed, chunk).
- * Errors: PP_ERR_INVALID (chunk out of range), PP_ERR_CUDA. */
+ * Collective for W > 1: every rank passes the same (seed, chunk).  With
+ * PP_PEERS_IPC each rank posts a hash of (seed, chunk) with a sequence number
+ * into its IPC-mapped flag word and reads every peer's (blocking until all
+ * ranks have called, PPLOAD_COLLECTIVE_TIMEOUT_S, default 300 s); with
+ * PP_PEERS_NCCL the hash is all-reduced.  Differing arguments return
+ * PP_ERR_INVALID on every rank and leave the previous epoch in place.
+ * PP_PEERS_NCCL also derives the epoch's per-step send / receive counts from
+ * the order here (one [steps][W][W] table, copied to the host).
+ * Errors: PP_ERR_INVALID (chunk out of range, arguments differ across ranks),
+ * PP_ERR_STATE (peers did not arrive in time), PP_ERR_CUDA, PP_ERR_NCCL. */
 pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream);
 
 /* Locality-aware alternative for sharded loaders ("data
@@ -239,8 +274,9 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk);
  * pp_next_batches_ev with per-buffer events.
  * When consumer_stream is the loader stream (pp_set_stream), consecutive
  * batches of one epoch may execute concurrently (programmatic dependent
- * launch): give each call its own buffer, or put the consumer's kernels
- * between two calls that reuse one.
+ * launch); the library only chains a launch whose out / labels / node-id
+ * ranges do not overlap those of the launches it would run beside, so a
+ * reused slot serialises instead of racing.
  * Errors: PP_ERR_STATE (no permute yet), PP_END_OF_EPOCH (*rows = 0),
  * PP_ERR_INVALID, PP_ERR_CUDA. */
 pp_status pp_next_batch(pp_loader* L, void* out, int32_t* out_labels, int64_t* out_nodes,
@@ -387,10 +423,21 @@ int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_byt
  * all-gathers the W handles (e.g. torch.distributed) and passes them,
  * rank-ordered, to pp_import_peer_stores on every rank. */
 pp_status pp_export_store(pp_loader* L, void* handle_out);
+/* The handle carries: the store's and the exchange copy's CUDA IPC handles, the
+ * IPC handle of the rank's collective flag words (pp_epoch_permute), the number
+ * of HBM rows, and -- when the rank spills -- the process id and descriptor of
+ * its shared spill file, which every peer maps and registers at import (so the
+ * importing ranks must run on the same host, as CUDA IPC already requires). */
 pp_status pp_import_peer_stores(pp_loader* L, const void* handles /* W*PP_IPC_HANDLE_BYTES bytes */);
 
 /* PP_PEERS_LOOPBACK: link W handles of one process (same device), rank-ordered. */
 pp_status pp_link_loopback(pp_loader* const* loaders, int32_t world_size);
+
+/* PP_PEERS_NCCL: write a fresh NCCL unique id (PP_NCCL_ID_BYTES) to out; one rank
+ * calls it and broadcasts the bytes.  libnccl.so.2 is loaded on first use (the
+ * copy already in the process, else PPLOAD_NCCL_LIB, else the system one).
+ * Errors: PP_ERR_INVALID (NULL), PP_ERR_NCCL (library missing / failure). */
+pp_status pp_nccl_unique_id(void* out);
 
 /* ---- test / bench only ---------------------------------------------------- */
 

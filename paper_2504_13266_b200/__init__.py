@@ -18,6 +18,7 @@ import numpy as np
 from ._abi import (  # noqa: F401
     PP_OK, PP_ERR_INVALID, PP_ERR_OOM, PP_ERR_CUDA, PP_ERR_NCCL, PP_ERR_STATE, PP_END_OF_EPOCH,
     PP_F32, PP_BF16, PP_F16, PP_MEM_HOST, PP_MEM_DEVICE, PP_MEM_FILES, PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK,
+    PP_PEERS_NCCL, IPC_HANDLE_BYTES, NCCL_ID_BYTES,
     pp_hop_desc, pp_loader_desc, pp_loader_info, PPError, lib, LIB_PATH,
 )
 
@@ -28,7 +29,7 @@ __all__ = [
     "pp_fill_synthetic", "pp_get_order", "pp_read_store", "pp_link_loopback", "pp_export_store",
     "pp_import_peer_stores", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
     "pp_epoch_permute_local", "pp_propagate_store", "pp_next_batches_ev",
-    "pp_set_grid_limit",
+    "pp_set_grid_limit", "pp_nccl_unique_id",
 ]
 
 
@@ -84,7 +85,7 @@ def pp_footprint_bytes(num_nodes, feat_dim, elem_bytes, num_ops, num_hops_R) -> 
 def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_dim, hop_stride=0, row_stride=0,
                      dtype=PP_F32, node_set=None, labels=None, batch_size, out_dtype=PP_BF16, drop_last=False,
                      hbm_budget_bytes=0, world_size=1, rank=0, peers=PP_PEERS_NONE, device=0, files=None,
-                     store_set_only=False, borrow_device_data=False):
+                     store_set_only=False, borrow_device_data=False, nccl_unique_id=None):
     """pp_loader_create(desc) -> handle.  ``data`` is a numpy array (host) or a torch CUDA tensor
     (device) of the hop matrices with the given element strides; None allocates the store only.
     ``files``: H hop file paths (raw [N][F] of dtype each) -> the storage tier (PP_MEM_FILES)."""
@@ -129,6 +130,10 @@ def pp_loader_create(*, data=None, where=PP_MEM_HOST, num_nodes, num_hops, feat_
     d.device = device
     d.store_set_only = int(store_set_only)
     d.borrow_device_data = int(borrow_device_data)
+    if nccl_unique_id is not None:
+        uid = ctypes.create_string_buffer(bytes(nccl_unique_id), NCCL_ID_BYTES)
+        keep.append(uid)
+        d.nccl_unique_id = ctypes.cast(uid, ctypes.c_void_p).value
     h = ctypes.c_void_p()
     _check(lib().pp_loader_create(ctypes.byref(d), ctypes.byref(h)), "pp_loader_create")
     return h
@@ -257,7 +262,11 @@ def pp_link_loopback(handles) -> None:
     _check(lib().pp_link_loopback(arr, len(handles)), "pp_link_loopback")
 
 
-IPC_HANDLE_BYTES = 128  # PP_IPC_HANDLE_BYTES
+def pp_nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (PP_NCCL_ID_BYTES) for PP_PEERS_NCCL loaders; broadcast it to every rank."""
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(lib().pp_nccl_unique_id(buf), "pp_nccl_unique_id")
+    return buf.raw
 
 
 def pp_export_store(h) -> bytes:

@@ -11,7 +11,9 @@ LIB_PATH = os.path.join(HERE, "libppload.so")
 PP_OK, PP_ERR_INVALID, PP_ERR_OOM, PP_ERR_CUDA, PP_ERR_NCCL, PP_ERR_STATE, PP_END_OF_EPOCH = range(7)
 PP_F32, PP_BF16, PP_F16 = 0, 1, 2
 PP_MEM_HOST, PP_MEM_DEVICE, PP_MEM_FILES = 0, 1, 2
-PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK = 0, 1, 2
+PP_PEERS_NONE, PP_PEERS_IPC, PP_PEERS_LOOPBACK, PP_PEERS_NCCL = 0, 1, 2, 3
+IPC_HANDLE_BYTES = 256  # PP_IPC_HANDLE_BYTES
+NCCL_ID_BYTES = 128  # PP_NCCL_ID_BYTES
 
 # every symbol include/pp_loader.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -20,7 +22,7 @@ EXPORTS = [
     "pp_export_store", "pp_import_peer_stores", "pp_link_loopback", "pp_fill_synthetic", "pp_get_order",
     "pp_read_store", "pp_debug_set_sort_bits_delta", "pp_next_batches_linear", "pp_propagate",
     "pp_epoch_permute_local", "pp_propagate_store", "pp_next_batches_ev",
-    "pp_set_grid_limit",
+    "pp_set_grid_limit", "pp_nccl_unique_id",
 ]
 
 
@@ -59,6 +61,7 @@ class pp_loader_desc(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("store_set_only", ctypes.c_int32),
         ("borrow_device_data", ctypes.c_int32),
+        ("nccl_unique_id", ctypes.c_void_p),
     ]
 
 
@@ -81,6 +84,13 @@ class pp_loader_info(ctypes.Structure):
         ("exchange_cast", ctypes.c_int32),
         ("storage_mode", ctypes.c_int32),
         ("storage_bytes_read", ctypes.c_int64),
+        ("pdl_launches", ctypes.c_int64),
+        ("all_to_all", ctypes.c_int32),
+        ("spill_shared", ctypes.c_int32),
+        ("hbm_store_bytes", ctypes.c_int64),
+        ("hbm_exchange_bytes", ctypes.c_int64),
+        ("hbm_scratch_bytes", ctypes.c_int64),
+        ("host_spill_bytes", ctypes.c_int64),
     ]
 
 
@@ -126,6 +136,7 @@ def lib():
                 "pp_propagate_store": (st, [P, i32, P, P, P, P]),
                 "pp_next_batches_ev": (st, [P, i32, P, i64, P, P, P, P, P, P]),
                 "pp_set_grid_limit": (st, [P, i32]),
+                "pp_nccl_unique_id": (st, [P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -187,6 +187,41 @@ cudaError_t file_tier_step(FileTier* T, int64_t step, int32_t in_dtype, int32_t 
                            uint8_t* out, int32_t* out_labels, int64_t* out_nodes, bool out_vec, cudaStream_t st,
                            int32_t* rows, std::string* err);
 
+// ---- all-to-all exchange (exchange.cu): the NCCL baseline of SURVEY.md §8(e) ----------------
+// n[t][d][o] (u32 [steps][W][W]): positions of slice d of step t whose row owner o holds.
+cudaError_t launch_a2a_counts(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t steps, int32_t B,
+                              int32_t W, uint32_t* table, cudaStream_t st);
+struct A2AIndexArgs {
+  const uint32_t* order;
+  const int64_t* node_set;  // row-space resolution as in GatherArgs (null for compact stores)
+  const int64_t* out_ids;   // compact stores: node ids / labels via out_ids[x]
+  const int32_t* labels;
+  int64_t N;                // positions of the epoch
+  int64_t step_pos0;        // first position of the step (t * W * B)
+  int32_t B, W;
+  int32_t self;             // owner whose local rows go to send_rows
+  int32_t slice_lo, slice_hi;  // destination slices handled (one CTA each)
+  int32_t recv_rank;        // slice whose receive index / ids / labels are written (-1: none)
+  int32_t send_off[kMaxWorld];  // row offset of segment d in send_rows
+  int32_t recv_off[kMaxWorld];  // row offset of owner o's rows in the receive buffer
+  uint32_t* send_rows;      // local rows of `self`, by destination segment, slice order
+  uint32_t* recv_src;       // [B]: receive-buffer row of slice position j
+  int32_t* out_labels;      // [B] or null
+  int64_t* out_nodes;       // [B] or null
+};
+cudaError_t launch_a2a_index(const A2AIndexArgs& a, cudaStream_t st);
+cudaError_t launch_a2a_unpack(const uint8_t* recv, const uint32_t* recv_src, int32_t rows, int64_t rec_out,
+                              uint8_t* out, bool vec, cudaStream_t st);
+// NCCL, loaded with dlopen on first use.
+bool nccl_unique_id(void* out128, std::string* err);
+void* nccl_comm_create(const void* id128, int W, int rank, std::string* err);
+void nccl_comm_destroy(void* comm, bool abort);
+bool nccl_check_async(void* comm, std::string* err);
+bool nccl_exchange(void* comm, int W, const uint8_t* send, const int64_t* send_off, const int64_t* send_bytes,
+                   uint8_t* recv, const int64_t* recv_off, const int64_t* recv_bytes, cudaStream_t st,
+                   std::string* err);
+bool nccl_same_everywhere(void* comm, int64_t h, int64_t* buf, cudaStream_t st, bool* same, std::string* err);
+
 // order (u32 positions) -> global node ids (int64), for pp_get_order.
 cudaError_t launch_order_to_nodes(const uint32_t* order, const int64_t* node_set, int64_t N, int64_t* dst,
                                   cudaStream_t st);

@@ -6,8 +6,13 @@
 // kernels of permute.cu / gather.cu; this file validates, allocates, lays out
 // and enqueues.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cerrno>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +20,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pp_loader.h"
@@ -67,17 +73,25 @@ struct pp_loader {
   bool borrowed = false;        // d_store is the caller's buffer (desc.borrow_device_data)
   uint8_t* h_spill = nullptr;
   uint8_t* d_spill = nullptr;  // device alias of h_spill
+  int spill_fd = -1;           // PP_PEERS_IPC spill: memfd shared with the peers (h_spill = its mapping)
+  size_t spill_bytes = 0;
+  struct PeerSpill {
+    void* p;
+    size_t bytes;
+  };
+  std::vector<PeerSpill> peer_spills;  // peers' spill files mapped + registered here
   uint8_t* d_xstore = nullptr;  // exchange copy: HBM rows cast to out_dtype, read by the peers (W > 1)
   int64_t xrec_stride = 0;      // its pitch (same on every rank; 0 when the dtype pair has no cast)
   int64_t* d_node_set = nullptr;
   int32_t* d_labels = nullptr;
   bool has_labels = false;
 
-  uint32_t* d_orders[2] = {nullptr, nullptr};  // current epoch + prefetched next epoch
+  uint32_t* d_orders[2] = {nullptr, nullptr};  // current epoch + prefetched next epoch (allocated at first prefetch)
   int cur = 0;
   uint32_t* d_order = nullptr;                  // == d_orders[cur]
   uint32_t* d_pi = nullptr;
   int64_t pi_cap = 0;
+  int64_t tmp_cap = 0;  // units SortScratch::tmp holds (allocated for the largest U seen)
   SortScratch sort{};
   int sort_bits_max = 0;
   int sort_bits_delta = 0;
@@ -125,6 +139,25 @@ struct pp_loader {
   ShardView shards[kMaxWorld]{};
   bool linked = false;
   std::vector<void*> ipc_opened;
+  // collective (seed, chunk) check of pp_epoch_permute (PP_PEERS_IPC): word[seq & 1] =
+  // (seq << 32) | hash, in device memory every peer maps
+  uint64_t* d_flags = nullptr;
+  const uint64_t* peer_flags[kMaxWorld]{};
+  uint32_t coll_seq = 0;
+  cudaStream_t cstream = nullptr;  // host <-> flag-word copies (never waits on other streams)
+  // all-to-all exchange (PP_PEERS_NCCL, or PP_PEERS_LOOPBACK with PPLOAD_EXCHANGE=a2a)
+  bool a2a = false;
+  void* nccl = nullptr;              // ncclComm_t
+  int64_t* d_nccl_scratch = nullptr;  // int64[2] for the argument check
+  uint32_t* d_counts = nullptr;      // [steps][W][W] of the current epoch
+  uint32_t* h_counts = nullptr;      // pinned host copy
+  int64_t counts_cap = 0;
+  uint32_t* d_send_rows = nullptr;
+  uint32_t* d_recv_src = nullptr;
+  uint8_t* d_sendbuf = nullptr;
+  uint8_t* d_recvbuf = nullptr;
+  int64_t pdl_launches = 0;
+  int64_t scratch_bytes = 0;  // HBM of order / sort / exchange buffers allocated so far
 
   // storage tier (hops.where == PP_MEM_FILES): no store; steps are read from the hop files
   FileTier* files = nullptr;
@@ -168,9 +201,29 @@ void release(pp_loader* L) {
   if (L->h_order_pin) cudaFreeHost(L->h_order_pin);
   cudaFree(L->d_stage);
   for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (const auto& ps : L->peer_spills) {
+    cudaHostUnregister(ps.p);
+    munmap(ps.p, ps.bytes);
+  }
+  if (L->nccl) nccl_comm_destroy(L->nccl, L->poisoned);
+  cudaFree(L->d_nccl_scratch);
+  cudaFree(L->d_counts);
+  if (L->h_counts) cudaFreeHost(L->h_counts);
+  cudaFree(L->d_send_rows);
+  cudaFree(L->d_recv_src);
+  cudaFree(L->d_sendbuf);
+  cudaFree(L->d_recvbuf);
+  cudaFree(L->d_flags);
+  if (L->cstream) cudaStreamDestroy(L->cstream);
   if (!L->borrowed) cudaFree(L->d_store);
   cudaFree(L->d_xstore);
-  if (L->h_spill) cudaFreeHost(L->h_spill);
+  if (L->spill_fd >= 0) {
+    cudaHostUnregister(L->h_spill);
+    munmap(L->h_spill, L->spill_bytes);
+    close(L->spill_fd);
+  } else if (L->h_spill) {
+    cudaFreeHost(L->h_spill);
+  }
   cudaFree(L->d_node_set);
   cudaFree(L->d_labels);
   if (L->pstream) cudaStreamSynchronize(L->pstream);
@@ -262,6 +315,37 @@ int prefetch_priority() {
   return least;
 }
 
+// Spill of an IPC-sharded loader: an anonymous shared-memory file (memfd), mapped MAP_SHARED here
+// and registered with CUDA (pinned, mapped); the peers open it through /proc/<pid>/fd/<fd>, map and
+// register it too (pp_import_peer_stores), so any rank reads any owner's spilled rows zero-copy
+// (host placement of data beyond GPU memory).
+bool alloc_shared_spill(pp_loader* L, size_t bytes, std::string* err) {
+  const int fd = memfd_create("ppload-spill", MFD_CLOEXEC);
+  if (fd < 0) {
+    *err = std::string("memfd_create: ") + strerror(errno);
+    return false;
+  }
+  void* p = MAP_FAILED;
+  if (ftruncate(fd, static_cast<off_t>(bytes)) == 0)
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  if (p == MAP_FAILED) {
+    *err = std::string("ftruncate / mmap of ") + std::to_string(bytes) + " bytes: " + strerror(errno);
+    close(fd);
+    return false;
+  }
+  const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    *err = std::string("cudaHostRegister: ") + cudaGetErrorString(e);
+    munmap(p, bytes);
+    close(fd);
+    return false;
+  }
+  L->h_spill = static_cast<uint8_t*>(p);
+  L->spill_fd = fd;
+  L->spill_bytes = bytes;
+  return true;
+}
+
 bool fast_div_ok(int64_t d) { return d > 0 && static_cast<uint64_t>(128) * d * d < (uint64_t(1) << 40); }
 
 pp_status validate(const pp_loader_desc* d) {
@@ -291,10 +375,15 @@ pp_status validate(const pp_loader_desc* d) {
   if (d->world_size < 1 || d->world_size > kMaxWorld)
     return fail(PP_ERR_INVALID, "world_size must be in [1, %d]", kMaxWorld);
   if (d->rank < 0 || d->rank >= d->world_size) return fail(PP_ERR_INVALID, "rank out of range");
-  if (!files && (d->world_size == 1) != (d->peers == PP_PEERS_NONE))
-    return fail(PP_ERR_INVALID, "peers must be PP_PEERS_NONE iff world_size == 1");
-  if (d->peers != PP_PEERS_NONE && d->peers != PP_PEERS_IPC && d->peers != PP_PEERS_LOOPBACK)
+  if (d->peers != PP_PEERS_NONE && d->peers != PP_PEERS_IPC && d->peers != PP_PEERS_LOOPBACK &&
+      d->peers != PP_PEERS_NCCL)
     return fail(PP_ERR_INVALID, "unknown peers mode");
+  if (!files && d->world_size == 1 && d->peers != PP_PEERS_NONE && d->peers != PP_PEERS_NCCL)
+    return fail(PP_ERR_INVALID, "world_size == 1 takes peers = PP_PEERS_NONE (or PP_PEERS_NCCL)");
+  if (!files && d->world_size > 1 && d->peers == PP_PEERS_NONE)
+    return fail(PP_ERR_INVALID, "world_size > 1 needs peers = IPC, LOOPBACK or NCCL");
+  if (d->peers == PP_PEERS_NCCL && !d->nccl_unique_id)
+    return fail(PP_ERR_INVALID, "PP_PEERS_NCCL needs nccl_unique_id (pp_nccl_unique_id, broadcast by the caller)");
   if (d->node_set) {
     if (d->num_set < 1 || d->num_set >= (int64_t(1) << 32)) return fail(PP_ERR_INVALID, "num_set out of range");
     for (int64_t i = 0; i < d->num_set; ++i)
@@ -318,6 +407,22 @@ cudaError_t refresh_exchange_copy(pp_loader* L) {
 
 pp_status ensure_sort_scratch(pp_loader* L, uint32_t U, int bits) {
   const size_t hist_need = L->sort.two_level ? two_level_hist_entries(U) : 0;
+  const bool grow_tmp = static_cast<int64_t>(U) > L->tmp_cap;
+  if (grow_tmp || bits > L->sort_bits_max || !L->sort.counts || hist_need > L->sort.hist_cap) {
+    // work on either stream may still use the scratch being replaced
+    if (L->stream) cudaStreamSynchronize(L->stream);
+    if (L->pstream) cudaStreamSynchronize(L->pstream);
+  }
+  if (grow_tmp) {  // unit ids grouped by bucket: U entries (U = N for SGD-RR, ceil(N / c) with chunks)
+    cudaFree(L->sort.tmp);
+    L->sort.tmp = nullptr;
+    L->scratch_bytes -= L->tmp_cap * 4;
+    L->tmp_cap = 0;
+    if (cudaMalloc(&L->sort.tmp, static_cast<size_t>(U) * 4) != cudaSuccess)
+      return fail(PP_ERR_OOM, "sort scratch allocation failed (%u units)", U);
+    L->tmp_cap = U;
+    L->scratch_bytes += L->tmp_cap * 4;
+  }
   if (bits > L->sort_bits_max || !L->sort.counts || hist_need > L->sort.hist_cap) {
     const int nbits = std::max(bits, L->sort_bits_max);
     const size_t hist_cap = std::max(hist_need, L->sort.hist_cap);
@@ -464,22 +569,21 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (cudaMemcpy(L->d_node_set, desc->node_set, L->N * 8, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "node_set upload"));
   }
-  // ---- placement: HBM budget, remainder spills to pinned mapped host memory
-  const int64_t scratch = L->N * 4 * 3 + (int64_t(1) << 26) + (L->has_labels ? L->N_total * 4 : 0);
+  // ---- placement: HBM budget, remainder spills to pinned mapped host memory.  The automatic
+  // budget leaves 2 GiB plus what this loader allocates next: labels, the epoch order and the sort
+  // scratch for U = N units (a prefetched second order is allocated at the first pp_epoch_prefetch).
+  const int64_t scratch = L->N * 4 * 2 + (int64_t(1) << 26) + (desc->labels ? L->N_total * 4 : 0);
   int64_t budget = desc->hbm_budget_bytes;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return bail(fail(PP_ERR_CUDA, "cudaMemGetInfo failed"));
-    budget = static_cast<int64_t>(fr) - (int64_t(2) << 30) - scratch - L->N_total * 4 - L->N * 8;
+    budget = static_cast<int64_t>(fr) - (int64_t(2) << 30) - scratch;
     if (budget < 0) budget = 0;
   }
   L->n_hbm = files ? 0 : budget < 0 ? 0 : std::min<int64_t>(L->local_rows, budget / L->rec_stride);
   if (desc->borrow_device_data && desc->hbm_budget_bytes == 0) L->n_hbm = L->local_rows;  // nothing to allocate
   if (files) L->local_rows = 0;
   L->n_spill = L->local_rows - L->n_hbm;
-  if (L->W > 1 && L->n_spill > 0 && desc->peers == PP_PEERS_IPC)
-    return bail(fail(PP_ERR_INVALID, "sharded (IPC) loaders need the whole shard in HBM (%lld rows spill)",
-                     (long long)L->n_spill));
 
   if (desc->borrow_device_data) {
     // the caller's node-major device tensor IS the store (no copy; it must outlive the loader)
@@ -495,9 +599,15 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   if (!L->borrowed && L->n_hbm > 0 && cudaMalloc(&L->d_store, static_cast<size_t>(L->n_hbm * L->rec_stride)) != cudaSuccess)
     return bail(fail(PP_ERR_OOM, "cudaMalloc of the %lld-byte HBM store failed", (long long)(L->n_hbm * L->rec_stride)));
   if (L->n_spill > 0) {
-    if (cudaHostAlloc(&L->h_spill, static_cast<size_t>(L->n_spill * L->rec_stride),
-                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
-      return bail(fail(PP_ERR_OOM, "pinned spill allocation of %lld bytes failed", (long long)(L->n_spill * L->rec_stride)));
+    const size_t bytes = static_cast<size_t>(L->n_spill * L->rec_stride);
+    if (L->W > 1 && desc->peers == PP_PEERS_IPC) {
+      std::string err;
+      if (!alloc_shared_spill(L, bytes, &err)) return bail(fail(PP_ERR_OOM, "shared spill: %s", err.c_str()));
+    } else {
+      if (cudaHostAlloc(&L->h_spill, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+        return bail(fail(PP_ERR_OOM, "pinned spill allocation of %lld bytes failed", (long long)bytes));
+      L->spill_bytes = bytes;
+    }
     if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->d_spill), L->h_spill, 0) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "cudaHostGetDevicePointer failed"));
   }
@@ -522,12 +632,10 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
     if (cudaMemcpy(L->d_labels, desc->labels, L->N_total * 4, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(PP_ERR_CUDA, "labels upload"));
   }
-  if (cudaMalloc(&L->d_orders[0], L->N * 4) != cudaSuccess || cudaMalloc(&L->d_orders[1], L->N * 4) != cudaSuccess ||
-      cudaMalloc(&L->sort.tmp, L->N * 4) != cudaSuccess || cudaMalloc(&L->sort.ragged, 4) != cudaSuccess)
-    return bail(fail(PP_ERR_OOM, "order / sort scratch allocation"));
+  if (cudaMalloc(&L->d_orders[0], L->N * 4) != cudaSuccess || cudaMalloc(&L->sort.ragged, 4) != cudaSuccess)
+    return bail(fail(PP_ERR_OOM, "order allocation"));
+  L->scratch_bytes += L->N * 4;
   L->d_order = L->d_orders[0];
-  st = ensure_sort_scratch(L, static_cast<uint32_t>(L->N), sort_bucket_bits(L->N, 0));
-  if (st != PP_OK) return bail(st);
   if (cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(PP_ERR_CUDA, "stream creation"));
   L->own_stream = true;
@@ -560,8 +668,12 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   L->tma_ok = L->vector_path && gather_tma_ok(L->HF, L->in_dtype);
   L->shards[L->rank] = ShardView{L->d_store, L->d_spill, L->n_hbm};
   L->linked = (L->W == 1) || files;
+  // ---- all-to-all exchange (NCCL baseline; loopback emulation with PPLOAD_EXCHANGE=a2a)
+  const char* xenv = getenv("PPLOAD_EXCHANGE");
+  L->a2a = !files && (desc->peers == PP_PEERS_NCCL ||
+                      (desc->peers == PP_PEERS_LOOPBACK && xenv && !strcmp(xenv, "a2a")));
   // ---- exchange copy for the peers (see pp_loader.h): only if it fits after everything else
-  if (L->W > 1 && L->in_dtype == PP_F32 && L->out_dtype != PP_F32 && L->vector_path) {
+  if (L->W > 1 && !L->a2a && L->in_dtype == PP_F32 && L->out_dtype != PP_F32 && L->vector_path) {
     L->xrec_stride = (L->rec_out + 15) / 16 * 16;
     const char* env = getenv("PPLOAD_EXCHANGE_CAST");
     size_t fr = 0, tot = 0;
@@ -573,7 +685,21 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
         return bail(fail(PP_ERR_CUDA, "exchange copy: %s", cudaGetErrorString(e_x)));
     }
   }
+  // ---- collective argument check: flag words the peers map (PP_PEERS_IPC)
+  if (L->W > 1 && desc->peers == PP_PEERS_IPC) {
+    if (cudaMalloc(&L->d_flags, 64) != cudaSuccess || cudaMemset(L->d_flags, 0, 64) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&L->cstream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(PP_ERR_CUDA, "collective flag words"));
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PP_ERR_CUDA, "create sync"));
+  if (desc->peers == PP_PEERS_NCCL && !files) {  // collective: every rank's create joins here
+    if (cudaMalloc(&L->d_nccl_scratch, 16) != cudaSuccess) return bail(fail(PP_ERR_OOM, "NCCL scratch"));
+    std::string err;
+    L->nccl = nccl_comm_create(desc->nccl_unique_id, L->W, L->rank, &err);
+    if (!L->nccl) return bail(fail(PP_ERR_NCCL, "%s", err.c_str()));
+    L->linked = true;
+  }
+  L->desc.nccl_unique_id = nullptr;
   *out = L;
   return PP_OK;
 }
@@ -595,6 +721,8 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
   if (k < 1 || k >= L->H) return fail(PP_ERR_INVALID, "hop slot k = %d must be in [1, H-1 = %d]", k, L->H - 1);
   if (L->F > 256) return fail(PP_ERR_INVALID, "F = %d > 256", L->F);
   if (!L->linked) return fail(PP_ERR_STATE, "sharded loader not linked to its peers yet");
+  if (L->W > 1 && L->desc.peers == PP_PEERS_NCCL)
+    return fail(PP_ERR_INVALID, "pp_propagate_store reads the peers' stores: needs PP_PEERS_IPC or LOOPBACK");
   DevGuard g(L->dev);
   cudaStream_t user = static_cast<cudaStream_t>(stream);
   if (user != L->stream) {  // order after this loader's gathers (they read the store) ...
@@ -660,10 +788,15 @@ static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint3
     PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort_bits_delta == 0, L->sort, order, nullptr, st));
   } else {
     if (L->pi_cap < U) {
+      cudaStreamSynchronize(L->stream);  // either stream may still read the old buffer
+      cudaStreamSynchronize(L->pstream);
       cudaFree(L->d_pi);
       L->d_pi = nullptr;
+      L->scratch_bytes -= L->pi_cap * 4;
+      L->pi_cap = 0;
       if (cudaMalloc(&L->d_pi, static_cast<size_t>(U) * 4) != cudaSuccess) return fail(PP_ERR_OOM, "pi allocation");
       L->pi_cap = U;
+      L->scratch_bytes += L->pi_cap * 4;
     }
     PPL_CUDA(L, launch_unit_permutation(seed, U, bits, L->sort_bits_delta == 0, L->sort, L->d_pi, L->sort.ragged, st));
     PPL_CUDA(L, launch_chunk_expand(L->d_pi, U, static_cast<uint64_t>(n), static_cast<uint64_t>(chunk),
@@ -711,11 +844,101 @@ pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, voi
   return PP_OK;
 }
 
+// 32-bit digest of an epoch's collective arguments (splitmix64 finaliser over seed and chunk).
+static uint32_t epoch_arg_hash(uint64_t seed, int64_t chunk) {
+  uint64_t z = seed ^ (static_cast<uint64_t>(chunk) * 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<uint32_t>(z ^ (z >> 32));
+}
+
+// pp_epoch_permute is collective: every rank must pass the same (seed, chunk), or the ranks' slices
+// of "the" global permutation would overlap and leave gaps.  NCCL: all-reduce of the digest.  IPC:
+// each rank posts (seq << 32 | digest) into word seq & 1 of its flag words and reads every peer's
+// same word until it carries seq (a peer is at most one epoch ahead, and then writes the other
+// word).  Loopback shards share one caller, which drives them all.
+static pp_status check_epoch_args(pp_loader* L, uint64_t seed, int64_t chunk) {
+  const uint32_t h = epoch_arg_hash(seed, chunk);
+  if (L->nccl) {
+    bool same = false;
+    std::string err;
+    if (!nccl_same_everywhere(L->nccl, h, L->d_nccl_scratch, L->stream, &same, &err)) {
+      L->poisoned = true;
+      return fail(PP_ERR_NCCL, "epoch argument check: %s", err.c_str());
+    }
+    return same ? PP_OK : fail(PP_ERR_INVALID, "pp_epoch_permute arguments (seed, chunk) differ across ranks");
+  }
+  if (L->W == 1 || L->desc.peers != PP_PEERS_IPC || !L->d_flags) return PP_OK;
+  if (!L->linked) return fail(PP_ERR_STATE, "sharded loader: peers not linked yet");
+  const uint32_t seq = ++L->coll_seq;
+  const int slot = static_cast<int>(seq & 1u);
+  uint64_t word = (static_cast<uint64_t>(seq) << 32) | h;
+  PPL_CUDA(L, cudaMemcpyAsync(L->d_flags + slot, &word, 8, cudaMemcpyHostToDevice, L->cstream));
+  PPL_CUDA(L, cudaStreamSynchronize(L->cstream));
+  double limit_s = 300.0;
+  if (const char* e = getenv("PPLOAD_COLLECTIVE_TIMEOUT_S")) limit_s = atof(e);
+  const auto t0 = std::chrono::steady_clock::now();
+  int bad = -1;
+  for (int o = 0; o < L->W; ++o) {
+    if (o == L->rank) continue;
+    for (int polls = 0;; ++polls) {
+      uint64_t w = 0;
+      PPL_CUDA(L, cudaMemcpyAsync(&w, L->peer_flags[o] + slot, 8, cudaMemcpyDeviceToHost, L->cstream));
+      PPL_CUDA(L, cudaStreamSynchronize(L->cstream));
+      if (static_cast<uint32_t>(w >> 32) == seq) {
+        if (static_cast<uint32_t>(w) != h && bad < 0) bad = o;
+        break;
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit_s) {
+        // this epoch did not happen: retract the posted word so a later attempt is not matched against it
+        const uint64_t zero = 0;
+        PPL_CUDA(L, cudaMemcpyAsync(L->d_flags + slot, &zero, 8, cudaMemcpyHostToDevice, L->cstream));
+        PPL_CUDA(L, cudaStreamSynchronize(L->cstream));
+        --L->coll_seq;
+        return fail(PP_ERR_STATE, "rank %d did not reach pp_epoch_permute #%u within %.0f s", o, seq, limit_s);
+      }
+      if (polls > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
+  if (bad >= 0)
+    return fail(PP_ERR_INVALID, "pp_epoch_permute arguments (seed, chunk) differ across ranks (rank %d vs rank %d)",
+                L->rank, bad);
+  return PP_OK;
+}
+
+// All-to-all epochs: n[t][d][o] for every step of the epoch, on the host (sizes every send / recv).
+static pp_status build_a2a_counts(pp_loader* L) {
+  const int64_t need = L->steps_global * L->W * L->W;
+  if (need > L->counts_cap) {
+    cudaFree(L->d_counts);
+    if (L->h_counts) cudaFreeHost(L->h_counts);
+    L->d_counts = nullptr;
+    L->h_counts = nullptr;
+    L->scratch_bytes -= L->counts_cap * 4;
+    L->counts_cap = 0;
+    if (cudaMalloc(&L->d_counts, need * 4) != cudaSuccess ||
+        cudaHostAlloc(&L->h_counts, need * 4, cudaHostAllocDefault) != cudaSuccess)
+      return fail(PP_ERR_OOM, "exchange count table");
+    L->counts_cap = need;
+    L->scratch_bytes += need * 4;
+  }
+  PPL_CUDA(L, launch_a2a_counts(L->d_order, L->compact ? nullptr : L->d_node_set, L->N, L->steps_global,
+                                static_cast<int32_t>(L->B), L->W, L->d_counts, L->stream));
+  PPL_CUDA(L, cudaMemcpyAsync(L->h_counts, L->d_counts, need * 4, cudaMemcpyDeviceToHost, L->stream));
+  PPL_CUDA(L, cudaStreamSynchronize(L->stream));
+  return PP_OK;
+}
+
 pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream) {
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
   DevGuard g(L->dev);
+  {
+    const pp_status cs = check_epoch_args(L, seed, chunk);
+    if (cs != PP_OK) return cs;
+  }
   cudaStream_t user = static_cast<cudaStream_t>(stream);
   if (user != L->stream) {
     PPL_CUDA(L, cudaEventRecord(L->ev_in, user));
@@ -762,6 +985,10 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
     PPL_CUDA(L, cudaMemcpyAsync(L->h_order_pin, L->d_order, L->N * 4, cudaMemcpyDeviceToHost, L->stream));
     PPL_CUDA(L, cudaStreamSynchronize(L->stream));
   }
+  if (L->a2a) {
+    const pp_status cs = build_a2a_counts(L);
+    if (cs != PP_OK) return cs;
+  }
   L->local = false;
   L->steps = L->steps_global;
   L->last_kernel = pp_loader::kLastNone;
@@ -778,6 +1005,11 @@ pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
   if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
   DevGuard g(L->dev);
   if (L->pref_pending) PPL_CUDA(L, cudaStreamWaitEvent(L->pstream, L->ev_pref, 0));
+  if (!L->d_orders[L->cur ^ 1]) {  // the second order buffer: allocated at the first prefetch
+    if (cudaMalloc(&L->d_orders[L->cur ^ 1], L->N * 4) != cudaSuccess)
+      return fail(PP_ERR_OOM, "prefetch order buffer (%lld bytes)", (long long)(L->N * 4));
+    L->scratch_bytes += L->N * 4;
+  }
   // WAR on the spare order buffer (read by the previous epoch's batches) and on
   // the sort scratch (used by work already enqueued on the loader stream)
   PPL_CUDA(L, cudaEventRecord(L->ev_pref_in, L->stream));
@@ -923,12 +1155,116 @@ static pp_status enqueue_gather_steps(pp_loader* L, int64_t nsteps, const StepOu
                                     span(o.labels, nsteps * L->B * 4), span(o.nodes, nsteps * L->B * 8)};
   const bool pdl = chain_pdl(L, pp_loader::kLastGather, spans);
   PPL_CUDA(L, launch_gather(a, path, pdl, L->grid_per_sm, L->stream));
+  L->pdl_launches += pdl ? 1 : 0;
   // the next gather may overlap this one unless an event record follows it (pdl_ok false)
   L->last_kernel = pdl_ok ? pp_loader::kLastGather : pp_loader::kLastNone;
   for (int64_t i = 0; i < nsteps; ++i) {
     const int64_t s0 = a.first_pos + i * a.step_stride;
     o.rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - s0)));
   }
+  return PP_OK;
+}
+
+// All-to-all steps (SURVEY.md §8(e) NCCL baseline, exchange.cu): per step, a stable compaction of
+// every slice by owner (k_a2a_index), the pack of this rank's rows for every destination with the
+// loader's gather kernel (cast fused), ncclSend / ncclRecv of the segments (sizes from the epoch's
+// count table), and the unpack into batch order.  Loopback shards (PPLOAD_EXCHANGE=a2a) run each
+// owner's index + pack inside this call, writing straight into this rank's receive buffer.
+static pp_status enqueue_a2a_steps(pp_loader* L, int64_t nsteps, const StepOut& o) {
+  const int W = L->W, r = L->rank;
+  const int64_t B = L->B;
+  if (!L->d_recvbuf) {
+    const int64_t send_rows = L->nccl ? W * B : B;
+    if (cudaMalloc(&L->d_recv_src, B * 4) != cudaSuccess || cudaMalloc(&L->d_send_rows, send_rows * 4) != cudaSuccess ||
+        cudaMalloc(&L->d_recvbuf, B * L->rec_out) != cudaSuccess ||
+        (L->nccl && cudaMalloc(&L->d_sendbuf, send_rows * L->rec_out) != cudaSuccess))
+      return fail(PP_ERR_OOM, "all-to-all exchange buffers");
+    L->scratch_bytes += B * 4 + send_rows * 4 + B * L->rec_out + (L->nccl ? send_rows * L->rec_out : 0);
+  }
+  const bool unpack_vec = o.aligned && L->rec_out % 16 == 0;
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const int64_t t = L->cursor + i;
+    const uint32_t* n = L->h_counts + t * W * W;  // n[d * W + o]
+    A2AIndexArgs a{};
+    a.order = L->d_order;
+    a.node_set = L->compact ? nullptr : L->d_node_set;
+    a.out_ids = L->compact ? L->d_node_set : nullptr;
+    a.labels = L->d_labels;
+    a.N = L->N;
+    a.step_pos0 = t * W * B;
+    a.B = static_cast<int32_t>(B);
+    a.W = W;
+    a.send_rows = L->d_send_rows;
+    a.recv_src = L->d_recv_src;
+    a.out_labels = o.labels ? o.labels + i * B : nullptr;
+    a.out_nodes = o.nodes ? o.nodes + i * B : nullptr;
+    int32_t rows = 0;
+    for (int q = 0; q < W; ++q) {
+      a.recv_off[q] = rows;
+      rows += static_cast<int32_t>(n[r * W + q]);
+    }
+    // the pack: the loader's gather over a list of local rows of one owner (W = 1 view of its shard)
+    auto pack = [&](int owner, int64_t count, uint8_t* dst) -> pp_status {
+      GatherArgs g{};
+      g.order = L->d_send_rows;
+      g.N = count;
+      g.B = static_cast<int32_t>(count);
+      g.nsteps = 1;
+      g.out = dst;
+      g.W = 1;
+      g.shards[0] = ShardView{L->shards[owner].hbm, L->shards[owner].spill, L->shards[owner].n_hbm, nullptr};
+      g.rec_stride = L->rec_stride;
+      g.HF = L->HF;
+      g.in_dtype = L->in_dtype;
+      g.out_dtype = L->out_dtype;
+      g.tile_rows = L->tile_rows;
+      g.num_sms = L->num_sms;
+      g.max_ctas = L->max_ctas;
+      if (count > 0)
+        PPL_CUDA(L, launch_gather(g, L->vector_path ? kPathVector : kPathScalar, false, L->grid_per_sm, L->stream));
+      return PP_OK;
+    };
+    if (L->nccl) {
+      int64_t send_off[kMaxWorld], send_bytes[kMaxWorld], recv_off[kMaxWorld], recv_bytes[kMaxWorld];
+      int32_t total = 0;
+      for (int d = 0; d < W; ++d) {
+        a.send_off[d] = total;
+        send_off[d] = static_cast<int64_t>(total) * L->rec_out;
+        send_bytes[d] = static_cast<int64_t>(n[d * W + r]) * L->rec_out;
+        total += static_cast<int32_t>(n[d * W + r]);
+        recv_off[d] = static_cast<int64_t>(a.recv_off[d]) * L->rec_out;
+        recv_bytes[d] = static_cast<int64_t>(n[r * W + d]) * L->rec_out;
+      }
+      a.self = r;
+      a.slice_lo = 0;
+      a.slice_hi = W;
+      a.recv_rank = r;
+      PPL_CUDA(L, launch_a2a_index(a, L->stream));
+      pp_status ps = pack(r, total, L->d_sendbuf);
+      if (ps != PP_OK) return ps;
+      std::string err;
+      if (!nccl_exchange(L->nccl, W, L->d_sendbuf, send_off, send_bytes, L->d_recvbuf, recv_off, recv_bytes, L->stream,
+                         &err)) {
+        L->poisoned = true;
+        return fail(PP_ERR_NCCL, "%s", err.c_str());
+      }
+    } else {  // loopback emulation: owner q packs its rows of slice r into the receive buffer
+      for (int q = 0; q < W; ++q) {
+        a.self = q;
+        a.slice_lo = r;
+        a.slice_hi = r + 1;
+        a.recv_rank = q == 0 ? r : -1;
+        for (int d = 0; d < W; ++d) a.send_off[d] = 0;
+        PPL_CUDA(L, launch_a2a_index(a, L->stream));
+        pp_status ps = pack(q, n[r * W + q], L->d_recvbuf + static_cast<int64_t>(a.recv_off[q]) * L->rec_out);
+        if (ps != PP_OK) return ps;
+      }
+    }
+    PPL_CUDA(L, launch_a2a_unpack(L->d_recvbuf, L->d_recv_src, rows, L->rec_out, o.out + i * o.stride, unpack_vec,
+                                  L->stream));
+    o.rows[i] = rows;
+  }
+  L->last_kernel = pp_loader::kLastNone;
   return PP_OK;
 }
 
@@ -970,7 +1306,8 @@ static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stri
   const bool signals = handoff || (ho.events && ho.ready_ev);  // an event record follows the steps
   pp_status st = L->files ? enqueue_file_steps(L, nsteps, o)
                  : L->dma_epoch ? enqueue_dma_steps(L, nsteps, o)
-                                : enqueue_gather_steps(L, nsteps, o, !signals);
+                 : (L->a2a && !L->local) ? enqueue_a2a_steps(L, nsteps, o)
+                                         : enqueue_gather_steps(L, nsteps, o, !signals);
   if (st != PP_OK) return st;
   // ---- loader -> consumer (RAW on `out`)
   if (handoff) {
@@ -1070,6 +1407,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   zspans[0].hi = zspans[0].lo + static_cast<uintptr_t>((nsteps - 1) * z_stride_bytes + L->B * L->H * D * z_elem);
   const bool pdl = !handoff && chain_pdl(L, pp_loader::kLastLinear, zspans);
   PPL_CUDA(L, launch_gather_linear(a, pdl, L->stream));
+  L->pdl_launches += pdl ? 1 : 0;
   if (want_ts) {
     static uint64_t h[24 * 14 + 4 * 1024];
     PPL_CUDA(L, cudaMemcpyAsync(h, dbg_ts, sizeof(h), cudaMemcpyDeviceToHost, L->stream));
@@ -1135,6 +1473,13 @@ pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
   info->exchange_cast = L->d_xstore != nullptr ? 1 : 0;
   info->storage_mode = L->files ? (file_tier_direct(L->files) ? 1 : 2) : 0;
   info->storage_bytes_read = L->files ? file_tier_bytes_read(L->files) : 0;
+  info->pdl_launches = L->pdl_launches;
+  info->all_to_all = L->a2a ? 1 : 0;
+  info->spill_shared = L->spill_fd >= 0 ? 1 : 0;
+  info->hbm_store_bytes = L->borrowed ? 0 : L->n_hbm * L->rec_stride;
+  info->hbm_exchange_bytes = L->d_xstore ? L->n_hbm * L->xrec_stride : 0;
+  info->hbm_scratch_bytes = L->scratch_bytes;
+  info->host_spill_bytes = static_cast<int64_t>(L->spill_bytes);
   return PP_OK;
 }
 
@@ -1185,20 +1530,52 @@ pp_status pp_read_store(pp_loader* L, int64_t row0, int64_t n, void* dst_host) {
   return PP_OK;
 }
 
+// Exported handle (PP_IPC_HANDLE_BYTES = 256):
+//   [0, 64)    CUDA IPC handle of the HBM store (zeros if every row spills)
+//   [64, 128)  CUDA IPC handle of the exchange copy (zeros if none)
+//   [128, 192) CUDA IPC handle of the collective flag words
+//   [192, 256) HandleTail: rows in HBM, the shared spill file (owner pid + descriptor, bytes)
+struct HandleTail {
+  uint32_t magic;  // 'PPH6'
+  int32_t pid;
+  int32_t spill_fd;  // -1: no spill
+  int32_t pad;
+  int64_t n_hbm;
+  int64_t spill_bytes;
+};
+static_assert(sizeof(HandleTail) <= 64, "handle tail");
+constexpr uint32_t kHandleMagic = 0x36485050u;  // "PPH6"
+
 pp_status pp_export_store(pp_loader* L, void* handle_out) {
   if (!L || !handle_out) return fail(PP_ERR_INVALID, "NULL argument");
   if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_export_store needs PP_PEERS_IPC");
   DevGuard g(L->dev);
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64 && PP_IPC_HANDLE_BYTES == 128, "IPC handle layout");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64 && PP_IPC_HANDLE_BYTES == 256, "IPC handle layout");
+  uint8_t* o = static_cast<uint8_t*>(handle_out);
+  memset(o, 0, PP_IPC_HANDLE_BYTES);
   cudaIpcMemHandle_t h;
-  PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_store));
-  memcpy(handle_out, &h, 64);  // [0, 64): the store; [64, 128): the exchange copy, or zeros
-  memset(static_cast<uint8_t*>(handle_out) + 64, 0, 64);
+  if (L->d_store) {
+    PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_store));
+    memcpy(o, &h, 64);
+  }
   if (L->d_xstore) {
     PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_xstore));
-    memcpy(static_cast<uint8_t*>(handle_out) + 64, &h, 64);
+    memcpy(o + 64, &h, 64);
   }
+  if (L->d_flags) {
+    PPL_CUDA(L, cudaIpcGetMemHandle(&h, L->d_flags));
+    memcpy(o + 128, &h, 64);
+  }
+  HandleTail t{kHandleMagic, static_cast<int32_t>(getpid()), L->spill_fd, 0, L->n_hbm,
+               static_cast<int64_t>(L->spill_fd >= 0 ? L->spill_bytes : 0)};
+  memcpy(o + 192, &t, sizeof(t));
   return PP_OK;
+}
+
+static bool nonzero(const uint8_t* p, int n) {
+  for (int i = 0; i < n; ++i)
+    if (p[i]) return true;
+  return false;
 }
 
 pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
@@ -1206,27 +1583,64 @@ pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
   if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_import_peer_stores needs PP_PEERS_IPC");
   if (L->linked) return fail(PP_ERR_STATE, "peers already imported");
   DevGuard g(L->dev);
+  const int64_t R = L->compact ? L->N : L->N_total;
   for (int o = 0; o < L->W; ++o) {
     if (o == L->rank) continue;
     const uint8_t* rec = static_cast<const uint8_t*>(handles) + PP_IPC_HANDLE_BYTES * o;
+    HandleTail t;
+    memcpy(&t, rec + 192, sizeof(t));
+    if (t.magic != kHandleMagic) return fail(PP_ERR_INVALID, "handle %d is not a pp_export_store handle (ABI 6)", o);
+    const int64_t rows_o = (R - o + L->W - 1) / L->W;
+    if (t.n_hbm < 0 || t.n_hbm > rows_o || (t.n_hbm < rows_o && t.spill_bytes < (rows_o - t.n_hbm) * L->rec_stride))
+      return fail(PP_ERR_INVALID, "handle %d: inconsistent placement (%lld of %lld rows in HBM)", o, (long long)t.n_hbm,
+                  (long long)rows_o);
     cudaIpcMemHandle_t h;
-    memcpy(&h, rec, 64);
     void* p = nullptr;
-    PPL_CUDA(L, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    L->ipc_opened.push_back(p);
+    if (nonzero(rec, 64)) {
+      memcpy(&h, rec, 64);
+      PPL_CUDA(L, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      L->ipc_opened.push_back(p);
+    }
     void* x = nullptr;
-    bool has_x = false;
-    for (int i = 64; i < 128; ++i) has_x |= rec[i] != 0;
-    if (has_x && L->xrec_stride > 0) {  // the owner keeps an exchange copy: read remote rows from it
+    if (nonzero(rec + 64, 64) && L->xrec_stride > 0) {  // the owner keeps an exchange copy: read remote rows from it
       memcpy(&h, rec + 64, 64);
       PPL_CUDA(L, cudaIpcOpenMemHandle(&x, h, cudaIpcMemLazyEnablePeerAccess));
       L->ipc_opened.push_back(x);
     }
-    const int64_t R = L->compact ? L->N : L->N_total;
-    const int64_t rows_o = (R - o + L->W - 1) / L->W;  // whole shard in HBM (checked at create)
-    L->shards[o] = ShardView{static_cast<const uint8_t*>(p), nullptr, rows_o, static_cast<const uint8_t*>(x)};
+    if (nonzero(rec + 128, 64)) {
+      void* f = nullptr;
+      memcpy(&h, rec + 128, 64);
+      PPL_CUDA(L, cudaIpcOpenMemHandle(&f, h, cudaIpcMemLazyEnablePeerAccess));
+      L->ipc_opened.push_back(f);
+      L->peer_flags[o] = static_cast<const uint64_t*>(f);
+    }
+    uint8_t* spill_dev = nullptr;
+    if (t.spill_bytes > 0) {  // the owner's spilled rows: map its shared spill file and register it here
+      char path[64];
+      snprintf(path, sizeof(path), "/proc/%d/fd/%d", t.pid, t.spill_fd);
+      const int fd = open(path, O_RDWR | O_CLOEXEC);
+      if (fd < 0) return fail(PP_ERR_INVALID, "rank %d's spill (%s): %s", o, path, strerror(errno));
+      void* m = mmap(nullptr, static_cast<size_t>(t.spill_bytes), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      close(fd);
+      if (m == MAP_FAILED) return fail(PP_ERR_OOM, "mmap of rank %d's spill: %s", o, strerror(errno));
+      if (cudaHostRegister(m, static_cast<size_t>(t.spill_bytes), cudaHostRegisterMapped | cudaHostRegisterPortable) !=
+          cudaSuccess) {
+        munmap(m, static_cast<size_t>(t.spill_bytes));
+        return fail(PP_ERR_OOM, "cudaHostRegister of rank %d's spill failed", o);
+      }
+      L->peer_spills.push_back({m, static_cast<size_t>(t.spill_bytes)});
+      PPL_CUDA(L, cudaHostGetDevicePointer(reinterpret_cast<void**>(&spill_dev), m, 0));
+    }
+    L->shards[o] = ShardView{static_cast<const uint8_t*>(p), spill_dev, t.n_hbm, static_cast<const uint8_t*>(x)};
   }
   L->linked = true;
+  return PP_OK;
+}
+
+pp_status pp_nccl_unique_id(void* out) {
+  if (!out) return fail(PP_ERR_INVALID, "NULL argument");
+  std::string err;
+  if (!nccl_unique_id(out, &err)) return fail(PP_ERR_NCCL, "%s", err.c_str());
   return PP_OK;
 }
 

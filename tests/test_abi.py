@@ -52,8 +52,9 @@ def _header_define(name):
 
 
 def test_abi_version_and_footprint(pp):
-    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 5
-    assert pp.IPC_HANDLE_BYTES == _header_define("PP_IPC_HANDLE_BYTES")
+    assert pp.pp_abi_version() == _header_define("PP_ABI_VERSION") == 6
+    assert pp.IPC_HANDLE_BYTES == _header_define("PP_IPC_HANDLE_BYTES") == 256
+    assert pp.NCCL_ID_BYTES == _header_define("PP_NCCL_ID_BYTES") == 128
     # input expansion K(R+1)x: 400 GB at R = 3, K = 1 -> 1.6 TB
     n = 100_000_000
     assert pp.pp_footprint_bytes(n, 1000, 4, 1, 0) == 400 * 10**9
@@ -69,6 +70,9 @@ def test_abi_version_and_footprint(pp):
     (dict(world_size=2, rank=0, peers=0), "peers"),
     (dict(world_size=1, rank=1), "rank"),
     (dict(node_set=[0, 5, 10]), "out of range"),
+    (dict(peers=3), "nccl_unique_id"),
+    (dict(peers=1), "world_size == 1"),
+    (dict(peers=7), "unknown peers"),
 ])
 def test_invalid_descriptors(pp, kw, msg):
     base = dict(num_nodes=10, num_hops=2, feat_dim=4, batch_size=2)
