@@ -17,9 +17,13 @@ noted): per_batch_call, gather_only, consumer_fused_linear (§8(f)-1), e2e (host
 store over PCIe), double_buffer (§8(a) A6, subprocess), next_rows (§8(f)-2 propagation,
 §8(f)-3 storage tier, papers100M compact store; subprocesses), cpu_baseline (the oracle).
 
-N > 1 (torchrun): ogbn-papers100M-shaped (configs[2]): N = 111,059,956, F = 128, K = 3,
-B = 8192 per rank, chunk reshuffle c = 8192, nodes sharded round-robin over the ranks,
-rows read from the owners' HBM by NVLink peer loads (CUDA IPC).
+N > 1 (torchrun, one process per GPU): weak scaling of the same per-GPU work -- a products-shaped
+shard per rank (N_total = 2,449,029 x N), one global permutation, nodes sharded round-robin, the
+(N-1)/N remote rows of every batch read from the owners' HBM by NVLink peer loads (CUDA IPC; the
+owners keep cast exchange copies).  Secondary keys at N > 1: exchange_nccl (the same epochs with an
+NCCL all-to-all exchange, SURVEY.md §8(e)'s baseline), papers100M (configs[2]: N = 111,059,956,
+F = 128, c = 8192, sharded over the N ranks, strong scaling), e2e (every shard in shared pinned host
+memory), memory_plan (per rank), nvlink_peer_copy_GBs (the NVLink denominator, measured in the run).
 """
 from __future__ import annotations
 
@@ -149,7 +153,7 @@ def committed_traffic(name: str):
 
 
 # --------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
-def oracle_epoch_sample(cfg, nbatches: int, nthreads: int):
+def oracle_epoch_sample(cfg, nbatches: int, nthreads: int):  # noqa: D401
     """The oracle as it stands: permutation of all N units (qsort, 1 thread) + gather+cast of
     the first `nbatches` batches from a host store regenerated with the oracle generator (all rows,
     untimed).  Returns (extrapolated epoch seconds, timings)."""
@@ -231,10 +235,40 @@ def epoch_loop(L, seed, next_seed, chunk, steps, slots, slot_bytes, k, stream, n
             done += len(L.next_batches(n, slots[s0], slot_bytes, None, nodes, stream))
 
 
+def ring_plan(steps, per_call, slot_bytes, free_bytes, cap=4e9, reserve=2 << 30):
+    """Slots of the timed output ring: one per step of the epoch, at most `cap` bytes and at most the
+    HBM left after the store, the exchange copy and the order minus a reserve, but never fewer than
+    one launch's worth (per_call slots)."""
+    ring_bytes = max(per_call * slot_bytes, min(cap, free_bytes - reserve))
+    return int(min(steps, max(per_call, ring_bytes // slot_bytes)))
+
+
 def ring_slots(steps, per_call, slot_bytes):
     """Output ring of the timed loop: one slot per step of the epoch, capped at 4 GB (>= 1 GB >> L2,
     so the outputs go to DRAM)."""
     return min(steps, max(per_call, int(4e9 // slot_bytes)))
+
+
+def measure_peer_copy(torch, local, W, shared_gpu):
+    """NVLink denominator measured in this run: every rank copies 1 GiB from the next rank's GPU into
+    its own (cudaMemcpyPeer through torch, all ranks at once, so every GPU also serves one reader),
+    best of 5, CUDA events on the local device."""
+    if shared_gpu or W < 2:
+        return None
+    peer = (local + 1) % W
+    src = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{peer}")
+    dst = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{local}")
+    best = 0.0
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, (1 << 30) / (a.elapsed_time(b) / 1e3) / 1e9)
+    del src, dst
+    torch.cuda.empty_cache()
+    return best
 
 
 def run_ours(args):
@@ -257,43 +291,59 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    name = args.config or ("products" if W == 1 else "papers100M")
-    cfg = dict(CONFIGS[name])
-    if args.chunk is not None:
-        cfg["chunk"] = args.chunk
-    N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
     stream = torch.cuda.Stream()
+    k = max(1, args.per_call)
 
-    desc = dict(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
-                device=local)
-    if W > 1:
-        desc.update(world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
-    L = pp.Loader(**desc)
-    L.fill_synthetic(DATA_SEED)
-    if W > 1:
-        h = pp.pp_export_store(L.h)
-        hs = [None] * W
-        dist.all_gather_object(hs, h)
-        pp.pp_import_peer_stores(L.h, b"".join(hs))
-    L.set_stream(stream)
-    info = L.query()
-    steps = info["steps_per_epoch"]
-    rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
+    def gather_all(obj):
+        if not dist:
+            return [obj]
+        out = [None] * W
+        dist.all_gather_object(out, obj)
+        return out
 
-    slot_bytes = B * H * F * 2
-    nslots = ring_slots(steps, args.per_call, slot_bytes)
-    ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
-    slots = list(ring.unbind(0))  # slot views made once, not per call (torch indexing costs ~1 us)
-    # rows this rank assembles per epoch (for the algorithmic bytes)
-    my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
-    U = -(-N // chunk)
-    # kernels of ours per permutation: one-CTA sort (U <= 4096) or the 6-kernel bucket sort
-    # (+ ragged-chunk search), + the chunk expansion when chunk > 1
-    perm_kernels = (1 if U <= 4096 else 6 + (chunk > 1)) + (chunk > 1)
+    peer_gbs = measure_peer_copy(torch, local, W, shared_gpu)
+    peer_all = gather_all(peer_gbs)
+    peer_meas = [x for x in peer_all if x]
+    nvl_peak = statistics.median(peer_meas) if peer_meas else 770.0
+    nvl_kind = (f"measured in this run: peer copy into each rank from the next one, median over ranks "
+                f"{[round(x, 1) for x in peer_meas]}" if peer_meas else
+                "fallback: guide-measured peer copy per direction (B200_PROFILING.md), not measurable here")
 
-    def timed(k, nsteps, sampler_index=None):
+    def make_loader(cfg, mode="ipc", budget=0):
+        desc = dict(num_nodes=cfg["N"], num_hops=cfg["H"], feat_dim=cfg["F"], dtype=pp.PP_F32, batch_size=cfg["B"],
+                    out_dtype=pp.PP_BF16, device=local, hbm_budget_bytes=budget)
+        uid = None
+        if mode == "nccl":
+            uid = gather_all(pp.pp_nccl_unique_id() if rank == 0 else None)[0]
+            desc.update(peers=pp.PP_PEERS_NCCL, nccl_unique_id=uid, world_size=W, rank=rank)
+        elif W > 1:
+            desc.update(world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
+        L = pp.Loader(**desc)
+        L.fill_synthetic(DATA_SEED)
+        if W > 1 and mode == "ipc":
+            pp.pp_import_peer_stores(L.h, b"".join(gather_all(pp.pp_export_store(L.h))))
+        L.set_stream(stream)
+        return L
+
+    def measure(L, cfg, kk, nsteps, sampler_index=None, ring_cap=4e9, label=""):
+        """Timed epochs of bench.epoch_loop on loader L: returns the timing dict and the memory plan."""
+        N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
+        info = L.query()
+        steps = info["steps_per_epoch"]
+        rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
+        slot_bytes = B * H * F * 2
+        free, total = torch.cuda.mem_get_info()
+        nslots = ring_plan(steps, kk, slot_bytes, free, ring_cap)
+        ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
+        slots = list(ring.unbind(0))  # slot views made once, not per call (torch indexing costs ~1 us)
+        my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
+        plan = {"rank": rank, "device": local, "gpu_total": total, "gpu_free_before_ring": free,
+                "ring_bytes": nslots * slot_bytes, "ring_slots": nslots,
+                **{x: info[x] for x in ("rows_hbm", "rows_spill", "hbm_store_bytes", "hbm_exchange_bytes",
+                                        "hbm_scratch_bytes", "host_spill_bytes", "exchange_cast", "all_to_all")}}
+
         def epoch(e, ev_mid=None):
-            epoch_loop(L, SEED0 + e, SEED0 + e + 1 if args.prefetch else None, chunk, steps, slots, slot_bytes, k,
+            epoch_loop(L, SEED0 + e, SEED0 + e + 1 if args.prefetch else None, chunk, steps, slots, slot_bytes, kk,
                        stream, ev_mid=ev_mid)
 
         with torch.cuda.stream(stream):
@@ -326,117 +376,142 @@ def run_ours(args):
             tt = torch.tensor(t, device="cpu" if shared_gpu else "cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = tt.tolist()
-        launches, done = 0, 0  # gather launches per epoch (calls never wrap the ring)
+        launches, done = 0, 0  # batch launches per epoch (calls never wrap the ring)
         while done < steps:
-            done += 1 if k == 1 else min(k, steps - done, nslots - done % nslots)
+            done += 1 if kk == 1 else min(kk, steps - done, nslots - done % nslots)
             launches += 1
         per_launch_ms = t[1] / (nsteps * launches)
         bytes_per_launch = my_rows * (rec_in + rec_out + 4) / launches
+        del ring, slots
         return {"total_ms": t[0], "gather_ms": t[1], "perm_ms": t[2], "per_launch_ms": per_launch_ms,
                 "bytes_per_launch": bytes_per_launch, "achieved": bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
-                "launches": launches, "clocks": clk.summary() if clk is not None else None}
+                "launches": launches, "steps": steps, "nslots": nslots, "my_rows": my_rows, "rec_in": rec_in,
+                "rec_out": rec_out, "exchange_cast": info["exchange_cast"], "all_to_all": info["all_to_all"],
+                "clocks": clk.summary() if clk is not None else None, "plan": plan}
 
-    k = max(1, args.per_call)
-    m = timed(k, args.steps, sampler_index=local)
+    def nvlink_roofline(m, kernel):
+        # (W-1)/W of each rank's rows come from peers: from the owner's exchange copy (cast: rec_out
+        # bytes), its fp32 records (rec_in) without one, or packed + cast by the owner (a2a: rec_out)
+        rec_nvl = m["rec_out"] if (m["exchange_cast"] or m["all_to_all"]) else m["rec_in"]
+        nvl = m["my_rows"] / m["launches"] * rec_nvl * (W - 1) / W
+        achieved = nvl / (m["per_launch_ms"] / 1e3) / 1e9
+        return {"bound": "nvlink", "achieved": achieved, "peak": nvl_peak, "unit": "GB/s", "frac": achieved / nvl_peak,
+                "traffic": None, "kernel": kernel, "peak_kind": nvl_kind,
+                "algorithmic_nvlink_bytes_per_node": rec_nvl * (W - 1) / W, "hbm_GBs": m["achieved"],
+                "per_launch_us": m["per_launch_ms"] * 1e3,
+                "note": "per-launch time = CUDA-event span of the epoch's batch launches / launches, max over ranks"}
+
+    def finish(L):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()  # peers read this rank's store until every rank is done
+        L.close()
+        torch.cuda.empty_cache()
+
+    # ---- headline.  N = 1: products-shaped (configs[1]).  N > 1: weak scaling -- a products-shaped
+    # shard per rank (N_total = 2,449,029 x W), one global permutation, (W-1)/W of every batch read
+    # from the owners' HBM over NVLink (cast exchange copies) -- the per-GPU work of the N = 1 line.
+    name = args.config or "products"
+    cfg = dict(CONFIGS[name])
+    if args.chunk is not None:
+        cfg["chunk"] = args.chunk
+    if W > 1 and name == "products":
+        cfg["N"] = CONFIGS["products"]["N"] * W
+    N, chunk = cfg["N"], cfg["chunk"]
+    U = -(-N // chunk)
+    # kernels of ours per permutation: one-CTA sort (U <= 4096) or the 6-kernel bucket sort
+    # (+ ragged-chunk search), + the chunk expansion when chunk > 1
+    perm_kernels = (1 if U <= 4096 else 6 + (chunk > 1)) + (chunk > 1)
+    L = make_loader(cfg)
+    m = measure(L, cfg, k, args.steps, sampler_index=local)
+    plans = gather_all(m["plan"])
     ms_per_step = m["total_ms"] / args.steps
     value = N * args.steps / (m["total_ms"] / 1e3)  # all ranks together assemble N rows per epoch
     peak, peak_kind = peaks()
+    store_gb = N * m["rec_in"] / 1e9
     if W == 1:
         roofline = {"bound": "hbm", "achieved": m["achieved"], "peak": peak, "unit": "GB/s",
                     "frac": m["achieved"] / peak, "traffic": committed_traffic(f"gather_{name}_k{k}"),
                     "kernel": "k_gather_vec<bf16>", "peak_kind": peak_kind,
-                    "algorithmic_bytes_per_node": rec_in + rec_out + 4,
-                    "frac_of_8TBs_nominal": m["achieved"] / 8000.0}
+                    "algorithmic_bytes_per_node": m["rec_in"] + m["rec_out"] + 4,
+                    "frac_of_8TBs_nominal": m["achieved"] / 8000.0, "per_launch_us": m["per_launch_ms"] * 1e3,
+                    "algorithmic_bytes_per_launch": m["bytes_per_launch"],
+                    "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
+                            "(includes launch gaps and the overlapped next-epoch permutation)"}
     else:
-        # pull design: (W-1)/W of each rank's rows arrive over NVLink, read from the owner's
-        # exchange copy (already cast: rec_out bytes) or, without one, as fp32 records (rec_in)
-        rec_nvl = rec_out if L.query()["exchange_cast"] else rec_in
-        nvl = m["bytes_per_launch"] / (rec_in + rec_out + 4) * rec_nvl * (W - 1) / W
-        achieved = nvl / (m["per_launch_ms"] / 1e3) / 1e9
-        roofline = {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s", "frac": achieved / 770.0,
-                    "traffic": None, "kernel": "k_gather_tma<bf16, sharded>",
-                    "peak_kind": "guide-measured peer copy per direction (B200_PROFILING.md)",
-                    "algorithmic_nvlink_bytes_per_node": rec_nvl * (W - 1) / W, "hbm_GBs": m["achieved"],
-                    "exchange_cast": bool(L.query()["exchange_cast"])}
-    roofline.update({"per_launch_us": m["per_launch_ms"] * 1e3, "algorithmic_bytes_per_launch": m["bytes_per_launch"],
-                     "note": "per-launch time = CUDA-event span from the epoch's first gather to its last / launches "
-                             "(includes launch gaps and the overlapped next-epoch permutation)"})
+        roofline = nvlink_roofline(m, "k_gather_tma<bf16, sharded> (peer reads)")
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if W == 1 else "strong",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32->bf16", "data": "synthetic (§8(d) generator G, filled in place)",
-        "config": config_dict(name, cfg, W, "inputs > L2 (3.9 GB store), outputs rotate over a "
-                                            f"{ring.numel() * 2 / 1e9:.2f} GB ring of {nslots} slots"),
+        "config": config_dict(name if W == 1 else f"{name}-weak", cfg, W,
+                              f"inputs > L2 ({store_gb:.1f} GB store), outputs rotate over a "
+                              f"{m['nslots'] * cfg['B'] * cfg['H'] * cfg['F'] * 2 / 1e9:.2f} GB ring of "
+                              f"{m['nslots']} slots per rank"),
         "roofline": roofline, "gpu_launches": (perm_kernels + m["launches"]) * args.steps, "clocks": m["clocks"],
         "batches_per_launch": k, "prefetch_next_epoch_order": bool(args.prefetch),
         # SURVEY.md §8(d) timing protocol: (a) gather-only nodes/s (span of the epoch's gathers),
         # (b) whole epochs incl. the permutation (= value), (c) per-call latency (per_batch_call)
         "gather_only": {"value": N * args.steps / (m["gather_ms"] / 1e3), "unit": UNIT,
                         "ms_per_epoch": m["gather_ms"] / args.steps},
+        "memory_plan": plans,
     }
+    if W > 1:
+        result["nvlink_peer_copy_GBs"] = peer_all
     if k != 1 and not args.skip_k1:
-        m1 = timed(1, max(3, args.steps // 2))
+        n1 = max(3, args.steps // 2)
+        m1 = measure(L, cfg, 1, n1)
         result["per_batch_call"] = {
-            "value": N * max(3, args.steps // 2) / (m1["total_ms"] / 1e3), "unit": UNIT,
-            "ms_per_step": m1["total_ms"] / max(3, args.steps // 2), "achieved_GBs": m1["achieved"],
-            "per_call_us": m1["total_ms"] * 1e3 / (max(3, args.steps // 2) * steps),
+            "value": N * n1 / (m1["total_ms"] / 1e3), "unit": UNIT, "ms_per_step": m1["total_ms"] / n1,
+            "achieved_GBs": m1["achieved"], "per_call_us": m1["total_ms"] * 1e3 / (n1 * m1["steps"]),
             "note": "one pp_next_batch call (one launch) per batch from Python (Loader.next_batch fast path)"}
-    del ring, slots
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()  # peers read this rank's store until every rank is done
-    L.close()
-    torch.cuda.empty_cache()
+    finish(L)
 
-    if W > 1 and not args.skip_weak:
-        # Weak-scaling companion of the N = 1 headline: a products-shaped shard per rank
-        # (N_total = 2,449,029 x W), one global permutation, (W-1)/W of every batch read from
-        # peers -- the per-GPU work of the single-GPU line, so the two compare directly.
-        N = CONFIGS["products"]["N"] * W
-        H, F, B, chunk = CONFIGS["products"]["H"], CONFIGS["products"]["F"], CONFIGS["products"]["B"], 1
-        L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
-                      device=local, world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
-        L.fill_synthetic(DATA_SEED)
-        hs = [None] * W
-        dist.all_gather_object(hs, pp.pp_export_store(L.h))
-        pp.pp_import_peer_stores(L.h, b"".join(hs))
-        L.set_stream(stream)
-        info = L.query()
-        steps = info["steps_per_epoch"]
-        rec_in, rec_out = info["record_bytes_in"], info["record_bytes_out"]
-        slot_bytes = B * H * F * 2
-        nslots = min(steps, max(args.per_call, int(4e9 // slot_bytes)))
-        ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
-        slots = list(ring.unbind(0))
-        my_rows = sum(max(0, min(B, N - (t * W * B + rank * B))) for t in range(steps))
-        mw = timed(k, args.steps)
-        result["weak_products"] = {
-            "value": N * args.steps / (mw["total_ms"] / 1e3), "unit": UNIT, "num_nodes": N,
-            "ms_per_step": mw["total_ms"] / args.steps, "per_gpu_nodes_per_s": N * args.steps / (mw["total_ms"] / 1e3) / W,
-            "exchange_cast": bool(info["exchange_cast"]),
-            "note": "products-shaped shard per rank, global permutation, peer reads; same per-GPU work as N = 1"}
-        del ring, slots
-        torch.cuda.synchronize()
-        dist.barrier()
-        L.close()
-        torch.cuda.empty_cache()
-
+    if W > 1 and not args.skip_nccl:
+        # SURVEY.md §8(e) baseline on the same workload: every step's rows exchanged by an NCCL
+        # all-to-all (owner packs + casts, ncclSend/ncclRecv, receiver unpacks)
+        if shared_gpu:
+            result["exchange_nccl"] = {"unavailable": "NCCL refuses two ranks on one GPU (path check run)"}
+        else:
+            try:
+                L = make_loader(cfg, mode="nccl")
+                mn = measure(L, cfg, k, max(3, args.steps // 2))
+                result["exchange_nccl"] = {
+                    "value": N * max(3, args.steps // 2) / (mn["total_ms"] / 1e3), "unit": UNIT,
+                    "ms_per_step": mn["total_ms"] / max(3, args.steps // 2),
+                    "roofline": nvlink_roofline(mn, "pack (k_gather_vec) + ncclSend/ncclRecv + k_a2a_unpack"),
+                    "memory_plan": gather_all(mn["plan"])}
+                finish(L)
+            except Exception as e:  # the baseline must never break the headline
+                result["exchange_nccl"] = {"error": repr(e)[:300]}
+    if W > 1 and not args.skip_papers and shared_gpu:
+        result["papers100M"] = {"unavailable": "needs one GPU per rank (227 GB of shards; path check run)"}
+    elif W > 1 and not args.skip_papers:
+        # BASELINE configs[2]: papers100M-shaped, c = 8192, sharded over the W ranks (strong scaling)
+        pcfg = dict(CONFIGS["papers100M"])
+        try:
+            L = make_loader(pcfg)
+            mp_ = measure(L, pcfg, k, max(3, args.steps // 2))
+            result["papers100M"] = {
+                "value": pcfg["N"] * max(3, args.steps // 2) / (mp_["total_ms"] / 1e3), "unit": UNIT,
+                "ms_per_step": mp_["total_ms"] / max(3, args.steps // 2), "scaling": "strong",
+                "config": config_dict("papers100M", pcfg, W, "inputs > L2"),
+                "roofline": nvlink_roofline(mp_, "k_gather_tma<bf16, sharded> (peer reads)"),
+                "memory_plan": gather_all(mp_["plan"])}
+            finish(L)
+        except Exception as e:
+            result["papers100M"] = {"error": repr(e)[:300]}
+    if not args.skip_e2e:
+        result["e2e"] = e2e_host_store(pp, torch, CONFIGS["products"], args, W=W, rank=rank, local=local,
+                                       gather_all=gather_all, dist=dist, shared_gpu=shared_gpu)
     if W == 1 and name == "products" and not args.skip_consumer:
         result["consumer_fused_linear"] = consumer_fused_linear(pp, torch, cfg, args)
-    if W == 1 and not args.skip_e2e:
-        result["e2e"] = e2e_host_store(pp, torch, cfg, args)
     if W == 1 and name == "products" and not args.skip_double_buffer:
         result["double_buffer"] = double_buffer_secondary()
     if W == 1 and name == "products" and not args.skip_next_rows:
         result["next_rows"] = next_rows_secondary()
     if rank == 0 and W == 1 and not args.skip_cpu:
-        nthreads = os.cpu_count() or 1
-        s, inf = oracle_epoch_sample(cfg, 32, nthreads)
-        result["cpu_baseline"] = {
-            "value": N / s, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-            "sample": (f"full-N permutation (1 thread, qsort) + gather+cast of {inf['batches']} batches "
-                       f"({inf['gather_rows']} rows, {nthreads} OpenMP threads); epoch extrapolated by rows"),
-            "permute_s": inf["permute_s"], "gather_s": inf["gather_s"]}
+        result["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
         print(json.dumps(result))
     if dist:
@@ -551,31 +626,46 @@ def double_buffer_secondary():
         return {"error": repr(e)[:300]}
 
 
-def e2e_host_store(pp, torch, cfg, args):
-    """Same epoch with the hop store in pinned host memory (the paper's host placement,
-    PAPER.md:287-288): every feature byte crosses host->device inside the timed region
-    (UVA zero-copy reads), and each batch's node ids are read back to host."""
-    N, H, F, B, chunk = cfg["N"], cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
-    L = pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
-                  hbm_budget_bytes=-1)
+def e2e_host_store(pp, torch, cfg, args, W=1, rank=0, local=0, gather_all=None, dist=None, shared_gpu=False):
+    """The same epochs end to end from host memory (the paper's host placement):
+    the whole store in pinned host memory (N > 1: each rank's shard in a shared memfd spill that
+    every peer maps), read zero-copy over PCIe by the gather kernels, so every feature byte crosses
+    host -> device inside the timed region; each epoch's node ids are copied back to the host.
+    N > 1 uses the weak-scaling shard (products-shaped per rank)."""
+    N, H, F, B, chunk = cfg["N"] * W, cfg["H"], cfg["F"], cfg["B"], cfg["chunk"]
+    desc = dict(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16,
+                hbm_budget_bytes=-1, device=local)
+    if W > 1:
+        desc.update(world_size=W, rank=rank, peers=pp.PP_PEERS_IPC)
+    L = pp.Loader(**desc)
     L.fill_synthetic(DATA_SEED)
+    if W > 1:
+        pp.pp_import_peer_stores(L.h, b"".join(gather_all(pp.pp_export_store(L.h))))
     stream = torch.cuda.Stream()
     L.set_stream(stream)
     info = L.query()
     steps = info["steps_per_epoch"]
-    out = [torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    k = 8
+    nslots = min(steps, 2 * k)
+    ring = torch.empty((nslots, B, H, F), dtype=torch.bfloat16, device="cuda")
+    slots = list(ring.unbind(0))
     nodes = torch.empty((steps, B), dtype=torch.int64, device="cuda")
     host_nodes = torch.empty((steps, B), dtype=torch.int64, pin_memory=True)
 
     def epoch(e):
         L.epoch_permute(SEED0 + e, chunk, stream)
-        for t in range(steps):
-            L.next_batch(out[t % 2], None, nodes[t], stream)
+        done = 0
+        while done < steps:
+            s0 = done % nslots
+            n = min(k, steps - done, nslots - s0)
+            done += len(L.next_batches(n, slots[s0], B * H * F * 2, None, nodes[done], stream))
         host_nodes.copy_(nodes, non_blocking=True)
 
     with torch.cuda.stream(stream):
         epoch(0)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     reps = 2
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
@@ -586,10 +676,34 @@ def e2e_host_store(pp, torch, cfg, args):
         b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
+    if dist:
+        ms = max(gather_all(ms))
+        dist.barrier()
     L.close()
+    del ring, slots
+    torch.cuda.empty_cache()
     return {"value": N / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": N * info["record_bytes_in"],
-            "d2h_bytes_per_step": N * 8, "ms_per_step": ms,
-            "how": "store in pinned host memory, read zero-copy over PCIe by the gather kernel; node ids D2H"}
+            "d2h_bytes_per_step": N * 8, "ms_per_step": ms, "spill_shared": bool(info["spill_shared"]),
+            "how": "store in pinned host memory (N > 1: shared memfd spill mapped by every rank), read zero-copy "
+                   "over PCIe by the gather kernels, 8 batches per pp_next_batches call; node ids D2H per epoch"}
+
+
+def cpu_baseline(cfg):
+    """SURVEY.md §8(d) oracle timing in both modes: (i) 1 thread, the plain oracle; (ii) all host
+    cores (the gather+cast loops under omp parallel for).  Full-N permutation + a bounded sample of
+    batches, the epoch extrapolated by rows."""
+    nthreads = os.cpu_count() or 1
+    out = {}
+    for mode, nt, nb in (("one_thread", 1, 8), ("all_cores", nthreads, 32)):
+        s, inf = oracle_epoch_sample(cfg, nb, nt)
+        out[mode] = {"value": cfg["N"] / s, "threads": nt, "permute_s": inf["permute_s"], "gather_s": inf["gather_s"],
+                     "gather_rows": inf["gather_rows"]}
+    best = out["all_cores"]
+    return {"value": best["value"], "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": (f"full-N permutation (qsort, 1 thread) + gather+cast of {best['gather_rows']} rows "
+                       f"({nthreads} OpenMP threads; {out['one_thread']['gather_rows']} rows in the 1-thread mode); "
+                       "epoch extrapolated by rows"),
+            "modes": out}
 
 
 def main():
@@ -608,7 +722,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-consumer", action="store_true", help="skip the §8(f)-1 fused-linear measurement")
     ap.add_argument("--skip-double-buffer", action="store_true", help="skip the §8(a) A6 double-buffer measurement")
-    ap.add_argument("--skip-weak", action="store_true", help="N > 1: skip the products-shaped weak-scaling line")
+    ap.add_argument("--skip-nccl", action="store_true", help="N > 1: skip the NCCL all-to-all exchange line")
+    ap.add_argument("--skip-papers", action="store_true", help="N > 1: skip the papers100M (configs[2]) line")
     ap.add_argument("--skip-next-rows", action="store_true",
                     help="skip the §8(f) propagation / storage-tier / compact-store measurements")
     args = ap.parse_args()

@@ -23,3 +23,16 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "products-shaped"
+
+
+def test_ring_plan_fits_memory():
+    # the timed output ring: one slot per step, capped at 4 GB and at the HBM left after the store
+    import bench
+
+    slot = 8192 * 4 * 100 * 2  # products bf16 batch: 6.55 MB
+    assert bench.ring_plan(299, 8, slot, free_bytes=150e9) == 299  # whole epoch fits under the cap
+    assert bench.ring_plan(1695, 8, slot, free_bytes=150e9) == int(4e9 // slot)  # 4 GB cap
+    tight = (2 << 30) + 20 * slot
+    assert bench.ring_plan(1695, 8, slot, free_bytes=tight) == 20  # what is left after the reserve
+    assert bench.ring_plan(1695, 8, slot, free_bytes=1e9) == 8  # never below one launch's worth
+    assert bench.ring_plan(3, 8, slot, free_bytes=150e9) == 3

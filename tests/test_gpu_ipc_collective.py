@@ -142,3 +142,45 @@ def test_ipc_epoch_peer_timeout():
     res = _run("timeout")
     assert res[0]["status"] == pp.PP_ERR_STATE, res
     assert all(d["ok"] for d in res), res
+
+
+def test_shard_larger_than_hbm_spills_to_shared_host_memory():
+    """The memory plan at scale (configs[4]'s situation: a rank's shard exceeds its HBM): the
+    automatic budget keeps 2 GiB + the loader's own scratch free, the remaining rows go to the shared
+    spill, and records on both sides of the split hold the generator's values (O11)."""
+    import numpy as np
+    import torch
+
+    import __graft_entry__ as ge
+    import oracle
+
+    ge.build()
+    import paper_2504_13266_b200 as pp
+
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    H, F = 1, 1024
+    rec = H * F * 4
+    rows = (free + (3 << 30)) // rec  # 3 GiB more than the whole free HBM
+    N = 2 * rows
+    with pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=4096, out_dtype=pp.PP_BF16,
+                   world_size=2, rank=1, peers=pp.PP_PEERS_IPC) as L:
+        q = L.query()
+        assert q["local_rows"] == rows and q["rows_spill"] > 0 and q["spill_shared"] == 1
+        assert q["rows_hbm"] + q["rows_spill"] == rows
+        assert q["host_spill_bytes"] == q["rows_spill"] * rec
+        assert q["hbm_store_bytes"] <= free - (2 << 30) - N * 4  # order + sort scratch + reserve stay free
+        assert q["hbm_store_bytes"] >= free - (2 << 30) - 4 * N * 4 - (1 << 27)
+        L.fill_synthetic(2504)
+        for lr in (0, q["rows_hbm"] - 1, q["rows_hbm"], rows - 1):
+            got = L.read_store(int(lr), 1)[0].view(np.uint32)
+            assert np.array_equal(got, oracle.gen_rows(2504, oracle.F32, H, F, np.array([lr * 2 + 1]))[0].ravel())
+        L.epoch_permute_local(3, 1)  # this rank's own rows, HBM and spill: no peers needed
+        out = torch.empty((4096, H, F), dtype=torch.bfloat16, device="cuda")
+        nodes = torch.empty(4096, dtype=torch.int64, device="cuda")
+        assert L.next_batch(out, None, nodes) == 4096
+        torch.cuda.synchronize()
+        v = nodes.cpu().numpy()
+        assert np.all(v % 2 == 1)
+        want = oracle.cast_bf16(oracle.gen_rows(2504, oracle.F32, H, F, v))
+        assert np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16), want)
