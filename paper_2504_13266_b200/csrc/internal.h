@@ -143,8 +143,23 @@ struct StorePropArgs {
   uint8_t* xstore;          // own exchange copy or null: slot k rewritten with the cast
   int64_t xrec_stride;
   int32_t x_dtype;          // 1 bf16, 2 f16
+  const uint32_t* col32 = nullptr;  // int32 copy of col (the L2-sliced kernel), or null
 };
 cudaError_t launch_spmm_store(const StorePropArgs& a, cudaStream_t st);
+// col32[p] = col[p] (nnz entries; ids < 2^32), for the L2-sliced kernels.
+cudaError_t launch_col_to_u32(const int64_t* col, int64_t nnz, uint32_t* col32, cudaStream_t st);
+// deg[i] = row_ptr[i+1] - row_ptr[i] (hop-major propagation through the sliced kernel).
+cudaError_t launch_row_lengths(const int64_t* row_ptr, int64_t n, int32_t* deg, cudaStream_t st);
+// L2-sliced propagation (propagate.cu): a hop through a scratch of spmm_sliced_scratch_bytes
+// (fp64 weights per nonzero + a window-major copy of the input slot).  Hop-major: y = B x over n
+// rows of F fp32; fresh_w: compute the weights (else reuse the scratch's from the previous hop).
+cudaError_t launch_spmm_sliced_rows(int64_t n, int32_t F, const int64_t* row_ptr, const uint32_t* col32,
+                                   const int32_t* deg, const float* x, float* y, uint8_t* scratch, int64_t nnz,
+                                   bool fresh_w, cudaStream_t st);
+// Into a W = 1 loader store (slot a.k from slot a.k - 1; a.col32 required).
+cudaError_t launch_spmm_store_sliced(const StorePropArgs& a, uint8_t* scratch, int64_t nnz, cudaStream_t st);
+int64_t spmm_sliced_scratch_bytes(int64_t rows, int32_t F, int64_t nnz);
+bool spmm_use_sliced(int64_t rows, int32_t F);
 
 // ---- DMA-staged assembly (gather.cu): out row j = cast(stage record j) ----------
 // order: the step's order entries (positions -> node-set index or node id), for ids / labels.

@@ -157,6 +157,10 @@ struct pp_loader {
   uint8_t* d_sendbuf = nullptr;
   uint8_t* d_recvbuf = nullptr;
   int64_t pdl_launches = 0;
+  uint32_t* d_col32 = nullptr;  // int32 column ids for the L2-sliced propagation (pp_propagate_store)
+  int64_t col32_cap = 0;
+  uint8_t* d_xt = nullptr;      // its window-major copy of the input hop slot
+  int64_t xt_cap = 0;
   int64_t scratch_bytes = 0;  // HBM of order / sort / exchange buffers allocated so far
 
   // storage tier (hops.where == PP_MEM_FILES): no store; steps are read from the hop files
@@ -214,6 +218,8 @@ void release(pp_loader* L) {
   cudaFree(L->d_sendbuf);
   cudaFree(L->d_recvbuf);
   cudaFree(L->d_flags);
+  cudaFree(L->d_col32);
+  cudaFree(L->d_xt);
   if (L->cstream) cudaStreamDestroy(L->cstream);
   if (!L->borrowed) cudaFree(L->d_store);
   cudaFree(L->d_xstore);
@@ -487,6 +493,30 @@ pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64
       pools[dev] = pool;
     }
   }
+  if (spmm_use_sliced(n, F) && n < (int64_t(1) << 32) && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(hops) % 16 == 0) {
+    // L2-sliced passes (propagate.cu): int32 columns + degrees, weights recomputed per nonzero
+    uint32_t* col32 = nullptr;
+    int32_t* deg = nullptr;
+    uint8_t* xt = nullptr;
+    if (cudaMallocFromPoolAsync(reinterpret_cast<void**>(&col32), static_cast<size_t>(nnz) * 4, pools[dev], st) !=
+            cudaSuccess ||
+        cudaMallocFromPoolAsync(reinterpret_cast<void**>(&deg), static_cast<size_t>(n) * 4, pools[dev], st) !=
+            cudaSuccess ||
+        cudaMallocFromPoolAsync(reinterpret_cast<void**>(&xt),
+                                static_cast<size_t>(spmm_sliced_scratch_bytes(n, F, nnz)), pools[dev], st) != cudaSuccess)
+      return fail(PP_ERR_OOM, "propagation scratch (%lld nonzeros)", (long long)nnz);
+    e = launch_col_to_u32(col_idx, nnz, col32, st);
+    if (e == cudaSuccess) e = launch_row_lengths(row_ptr, n, deg, st);
+    for (int32_t k = 1; k <= K && e == cudaSuccess; ++k)
+      e = launch_spmm_sliced_rows(n, F, row_ptr, col32, deg, hops + (k - 1) * (plane / sizeof(float)),
+                                  hops + k * (plane / sizeof(float)), xt, nnz, k == 1, st);
+    cudaFreeAsync(col32, st);
+    cudaFreeAsync(deg, st);
+    cudaFreeAsync(xt, st);
+    if (e != cudaSuccess) return fail(PP_ERR_CUDA, "propagation: %s", cudaGetErrorString(e));
+    return PP_OK;
+  }
   if (cudaMallocFromPoolAsync(reinterpret_cast<void**>(&val), static_cast<size_t>(nnz) * sizeof(double), pools[dev],
                               st) != cudaSuccess)
     return fail(PP_ERR_OOM, "operator values (%lld nonzeros)", (long long)nnz);
@@ -743,7 +773,41 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
   a.xstore = L->d_xstore;
   a.xrec_stride = L->xrec_stride;
   a.x_dtype = L->out_dtype == PP_F16 ? 2 : 1;
-  PPL_CUDA(L, launch_spmm_store(a, user));
+  bool sliced = false;
+  int64_t nnz_sliced = 0;
+  if (L->W == 1 && spmm_use_sliced(L->N_total, L->F) && L->F % 4 == 0 && L->rec_stride % 16 == 0) {
+    // the L2-sliced kernel: int32 column ids (converted per call; the CSR may change) and a
+    // window-major copy of the input slot, both loader-owned scratch kept between calls
+    int64_t nnz = 0;
+    PPL_CUDA(L, cudaMemcpyAsync(&nnz, row_ptr + L->local_rows, 8, cudaMemcpyDeviceToHost, user));
+    PPL_CUDA(L, cudaStreamSynchronize(user));
+    const int64_t xt_bytes = spmm_sliced_scratch_bytes(L->local_rows, L->F, nnz);
+    if (nnz > L->col32_cap || xt_bytes > L->xt_cap) {
+      cudaFree(L->d_col32);
+      cudaFree(L->d_xt);
+      L->d_col32 = nullptr;
+      L->d_xt = nullptr;
+      L->scratch_bytes -= L->col32_cap * 4 + L->xt_cap;
+      L->col32_cap = L->xt_cap = 0;
+      if (cudaMalloc(&L->d_col32, static_cast<size_t>(nnz) * 4) == cudaSuccess &&
+          cudaMalloc(&L->d_xt, static_cast<size_t>(xt_bytes)) == cudaSuccess) {
+        L->col32_cap = nnz;
+        L->xt_cap = xt_bytes;
+        L->scratch_bytes += nnz * 4 + xt_bytes;
+      } else {  // no room: the row kernels read the int64 ids and the records directly
+        cudaFree(L->d_col32);
+        L->d_col32 = nullptr;
+        cudaGetLastError();
+      }
+    }
+    if (L->d_col32 && L->d_xt) {
+      PPL_CUDA(L, launch_col_to_u32(col_idx, nnz, L->d_col32, user));
+      a.col32 = L->d_col32;
+      sliced = true;
+      nnz_sliced = nnz;
+    }
+  }
+  PPL_CUDA(L, sliced ? launch_spmm_store_sliced(a, L->d_xt, nnz_sliced, user) : launch_spmm_store(a, user));
   if (user != L->stream) {  // ... and later loader work after this hop
     PPL_CUDA(L, cudaEventRecord(L->ev_out, user));
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_out, 0));

@@ -324,6 +324,272 @@ __global__ void __launch_bounds__(256) k_spmm_store(const StorePropArgs a) {
   }
 }
 
+// ---- L2-sliced propagation ----------------------------------------------------------------------
+// The neighbour reads of a hop are random rows of X_{k-1}: a products-sized hop reads ~50 GB of
+// 400-byte rows (126 M nonzeros) while X_{k-1} itself is 0.98 GB, so the row-per-warp kernels above
+// fetch most of it from DRAM again and again (ncu r1final: 64.9 GB of DRAM reads per hop).  The L2
+// allocates 128-byte lines, so a feature window of the node-major records (32 B of every 1600-B
+// record) would still occupy a whole line per row (313 MB at products size, more than the 126 MB
+// L2; measured r2: 185 GB of DRAM reads per hop).  So a hop first writes X_{k-1} window-major into a
+// scratch Xt[w][row][8 fp32] (k_slot_to_windows: one read of the slot, one write), then runs one
+// pass per 32-byte window: pass w gathers only Xt[w] -- rows x 32 B = 78 MB of fully used lines,
+// L2-resident after its first touch -- so DRAM carries X_{k-1} about twice plus the int32 column
+// ids and row pointers once per pass.  One thread per output row walks the row's nonzeros in
+// ascending column order with the window's features in fp64 registers: every output element is the
+// same sequence of separately rounded products and sums as before (bit-identical to the oracle, O3).
+// The weight 1/sqrt(d~_i d~_j) is recomputed per nonzero and pass (fp64 IEEE, as k_operator_values).
+constexpr int kWinBytes = 32;  // window pitch in xt: one L2 sector; 4 rows of a window share a 128-B line
+
+// Window width in bytes: 32 (default) or 16 (PPLOAD_SPMM_WINDOW=16: half the footprint, twice the passes).
+static int spmm_window() {
+  const char* e = getenv("PPLOAD_SPMM_WINDOW");
+  return (e && atoi(e) == 16) ? 16 : 32;
+}
+
+// Xt[w][r] (kWinBytes each, window w = bytes [32w, 32w + 32) of the slot) from slot bytes
+// [0, slot_bytes) of row r of `src` (rows < n_hbm at hbm + r * pitch + off, else spill).
+__global__ void k_slot_to_windows(const uint8_t* __restrict__ hbm, const uint8_t* __restrict__ spill, int64_t n_hbm,
+                                  int64_t rows, int64_t pitch, int64_t off, int32_t slot_bytes,
+                                  uint8_t* __restrict__ xt, int win) {
+  const int nwin = (slot_bytes + win - 1) / win;
+  const int vpr = slot_bytes / 16;  // float4 per row
+  // thread t -> (block of 64 rows, float4 v of the slot, row within the block): the slot's
+  // float4s of 64 rows are read by one CTA back to back (their lines stay in L2), and each
+  // window's 64 rows x 32 B are written contiguously
+  const int64_t total = (rows + 63) / 64 * 64 * vpr;  // whole 64-row blocks (the tail block is partial)
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t blk = t / (64 * vpr);
+    const int64_t rem = t - blk * 64 * vpr;
+    const int v = static_cast<int>(rem / 64);
+    const int64_t r = blk * 64 + (rem - static_cast<int64_t>(v) * 64);
+    if (r >= rows) continue;
+    const uint8_t* rec = r < n_hbm ? hbm + r * pitch : spill + (r - n_hbm) * pitch;
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(rec + off) + v);
+    const int w = v / (win / 16), c = v % (win / 16);
+    reinterpret_cast<float4*>(xt + (static_cast<int64_t>(w) * rows + r) * win)[c] = x;
+    (void)nwin;
+  }
+}
+
+// One pass: window `win` (nv float4 <= 2) of every output row.  Input: the compact window Xt[win]
+// (pitch kWinBytes).  Output: out rows (< out.n_hbm in out.hbm, else out.spill) at pitch out_pitch,
+// bytes out_off.. of the row; the owner's exchange copy (16-bit) at x_off when a.xstore is set.
+// L2 eviction policies: the window being gathered stays (evict_last); the per-pass streams of
+// column ids and weights, which would otherwise push it out of the L2, go first (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_u32_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_f64_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void ld_window(const void* p, int nv, float4& a, float4& b, uint64_t pol) {
+  if (nv > 1) {  // the whole 32-byte window in one 256-bit load (LDG.256)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p), "l"(pol));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                 : "l"(p), "l"(pol));
+    b = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmm_sliced(const StorePropArgs a, const double* __restrict__ wv,
+                                                     const uint8_t* __restrict__ xt_win, int win, int nv, ShardView out,
+                                                     int64_t out_pitch, int64_t out_off, int64_t x_off) {
+  constexpr int kU = 4;  // nonzeros loaded ahead of their accumulation
+  const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
+  for (int64_t lr = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; lr < a.local_rows;
+       lr += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = a.row_ptr[lr], e = a.row_ptr[lr + 1];
+    double acc[2][4];
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[v][c] = 0.0;
+    for (int64_t p0 = b; p0 < e; p0 += kU) {
+      const int m = static_cast<int>(min(static_cast<int64_t>(kU), e - p0));
+      uint32_t j[kU];
+      double wu[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        j[u] = u < m ? ld_u32_hint(a.col32 + p0 + u, stream) : 0u;
+        wu[u] = u < m ? ld_f64_hint(wv + p0 + u, stream) : 0.0;
+      }
+      float4 xv[kU][2];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (u < m) {
+          ld_window(xt_win + static_cast<int64_t>(j[u]) * win, nv, xv[u][0], xv[u][1], keep);
+        } else {
+          xv[u][0] = xv[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (u >= m) break;
+        const double w = wu[u];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          acc[v][0] = __dadd_rn(acc[v][0], __dmul_rn(w, static_cast<double>(xv[u][v].x)));
+          acc[v][1] = __dadd_rn(acc[v][1], __dmul_rn(w, static_cast<double>(xv[u][v].y)));
+          acc[v][2] = __dadd_rn(acc[v][2], __dmul_rn(w, static_cast<double>(xv[u][v].z)));
+          acc[v][3] = __dadd_rn(acc[v][3], __dmul_rn(w, static_cast<double>(xv[u][v].w)));
+        }
+      }
+    }
+    uint8_t* rec = const_cast<uint8_t*>(lr < out.n_hbm ? out.hbm + lr * out_pitch : out.spill + (lr - out.n_hbm) * out_pitch);
+    float4* yr = reinterpret_cast<float4*>(rec + out_off);
+    uint8_t* xr = (a.xstore != nullptr && lr < out.n_hbm) ? a.xstore + lr * a.xrec_stride + x_off : nullptr;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      if (v >= nv) break;
+      const float4 o = make_float4(__double2float_rn(acc[v][0]), __double2float_rn(acc[v][1]),
+                                   __double2float_rn(acc[v][2]), __double2float_rn(acc[v][3]));
+      yr[v] = o;
+      if (xr != nullptr) {
+        store_x16(xr + v * 8, a.x_dtype, o.x, o.y);
+        store_x16(xr + v * 8 + 4, a.x_dtype, o.z, o.w);
+      }
+    }
+  }
+}
+
+// w[p] = 1 / sqrt(d~_i d~_j) for every nonzero p of row i (column j): the oracle's O2 values (IEEE
+// fp64 multiply, sqrt, divide), computed once per call and streamed by every pass.
+__global__ void k_weights_from_deg(int64_t rows, const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col32,
+                                   const int32_t* __restrict__ deg, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < rows;
+       i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+    const double di = static_cast<double>(e - b);
+    for (int64_t p = b + lane; p < e; p += 32)
+      w[p] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(di, static_cast<double>(deg[col32[p]]))));
+  }
+}
+
+// Opt-in (PPLOAD_SPMM=sliced): measured slower than the row kernels on B200 at products size
+// (r2, profiles/r2/propagation_sliced.md: 23.5 ms vs 12.1 ms per hop).  A window read by every SM
+// is also cached in the reading die's L2 half, so a 78 MB window does not stay resident (54 % of
+// its sectors missed), and 16-byte windows (39 MB, 96 % hits) double the per-pass column / weight
+// streams instead (111 GB of DRAM reads per hop vs 65 GB for the row kernel).
+bool spmm_use_sliced(int64_t rows, int32_t F) {
+  (void)rows;
+  const char* e = getenv("PPLOAD_SPMM");
+  return e && !strcmp(e, "sliced") && F % 4 == 0;
+}
+
+int64_t spmm_sliced_scratch_bytes(int64_t rows, int32_t F, int64_t nnz) {
+  // window-major slot copy + int32 column ids + fp64 weights
+  return ((static_cast<int64_t>(F) * 4 + kWinBytes - 1) / kWinBytes) * rows * kWinBytes + nnz * 12 + 256;
+}
+
+// One hop through the window-major scratch: transpose slot (in) -> xt, then one pass per window.
+// scratch: [weights fp64 nnz][xt] (spmm_sliced_scratch_bytes); weights computed here when fresh_w.
+static cudaError_t run_sliced(const StorePropArgs& a, ShardView in, int64_t in_pitch, int64_t in_off, ShardView out,
+                              int64_t out_pitch, int64_t out_off, int64_t x_off, uint8_t* scratch, int64_t nnz,
+                              bool fresh_w, cudaStream_t st) {
+  const int32_t slot_bytes = a.F * 4;
+  const int64_t rows = a.local_rows;
+  const int win = spmm_window();
+  double* wv = reinterpret_cast<double*>(scratch);
+  uint8_t* xt = scratch + (nnz * 8 + 255) / 256 * 256;
+  if (fresh_w) {
+    const int64_t blocks = std::min<int64_t>((rows * 32 + 255) / 256, 148ll * 16);
+    k_weights_from_deg<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(rows, a.row_ptr, a.col32, a.deg, wv);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const int64_t total = (rows + 63) / 64 * 64 * (slot_bytes / 16);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148ll * 16);
+    k_slot_to_windows<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(in.hbm, in.spill, in.n_hbm, rows, in_pitch, in_off,
+                                                                      slot_bytes, xt, win);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const int nwin = (slot_bytes + win - 1) / win;
+  const int64_t blocks = std::min<int64_t>((rows + 255) / 256, 148ll * 8);
+  for (int w = 0; w < nwin; ++w) {
+    const int nv = std::min(win, slot_bytes - w * win) / 16;
+    k_spmm_sliced<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(a, wv, xt + static_cast<int64_t>(w) * rows * win, win,
+                                                                  nv, out, out_pitch, out_off + w * win,
+                                                                  x_off + w * (win / 2));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+__global__ void k_col_to_u32(const int64_t* __restrict__ col, int64_t nnz, uint32_t* __restrict__ col32) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    col32[p] = static_cast<uint32_t>(col[p]);
+}
+
+cudaError_t launch_col_to_u32(const int64_t* col, int64_t nnz, uint32_t* col32, cudaStream_t st) {
+  if (nnz <= 0) return cudaSuccess;
+  k_col_to_u32<<<148 * 16, 256, 0, st>>>(col, nnz, col32);
+  return cudaGetLastError();
+}
+
+__global__ void k_row_lengths(const int64_t* __restrict__ row_ptr, int64_t n, int32_t* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    deg[i] = static_cast<int32_t>(row_ptr[i + 1] - row_ptr[i]);
+}
+
+cudaError_t launch_row_lengths(const int64_t* row_ptr, int64_t n, int32_t* deg, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_row_lengths<<<148 * 8, 256, 0, st>>>(row_ptr, n, deg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_sliced_rows(int64_t n, int32_t F, const int64_t* row_ptr, const uint32_t* col32,
+                                   const int32_t* deg, const float* x, float* y, uint8_t* scratch, int64_t nnz,
+                                   bool fresh_w, cudaStream_t st) {
+  if (n <= 0 || F <= 0) return cudaSuccess;
+  if (F % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(y) % 16)
+    return cudaErrorInvalidValue;
+  StorePropArgs a{};
+  a.local_rows = n;
+  a.F = F;
+  a.row_ptr = row_ptr;
+  a.deg = deg;
+  a.col32 = col32;
+  const int64_t pitch = static_cast<int64_t>(F) * 4;
+  const ShardView in{reinterpret_cast<const uint8_t*>(x), nullptr, n};
+  const ShardView out{reinterpret_cast<const uint8_t*>(y), nullptr, n};
+  return run_sliced(a, in, pitch, 0, out, pitch, 0, 0, scratch, nnz, fresh_w, st);
+}
+
+cudaError_t launch_spmm_store_sliced(const StorePropArgs& a, uint8_t* scratch, int64_t nnz, cudaStream_t st) {
+  if (a.local_rows <= 0) return cudaSuccess;
+  if (a.W != 1 || a.col32 == nullptr || a.F % 4 != 0 || a.rec_stride % 16 != 0) return cudaErrorInvalidValue;
+  const ShardView me = a.shards[a.rank];
+  const int64_t slot = static_cast<int64_t>(a.F) * 4;
+  return run_sliced(a, me, a.rec_stride, (a.k - 1) * slot, me, a.rec_stride, a.k * slot,
+                    static_cast<int64_t>(a.k) * a.F * 2, scratch, nnz, true, st);
+}
+
 cudaError_t launch_spmm_store(const StorePropArgs& a, cudaStream_t st) {
   if (a.local_rows <= 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>((a.local_rows * 32 + 255) / 256, 148ll * 64);

@@ -32,6 +32,19 @@ row_ptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
 del rows
 nnz = int(row_ptr[-1])
 X = torch.randn((n, F), device="cuda", generator=g)
+# compulsory DRAM bytes of one hop: X_{k-1} read once, the column ids (int64, as given) and row
+# pointers once, X_k written once; the neighbour gathers (nnz rows of F*4 bytes) are L2 traffic when
+# the L2-sliced kernel keeps each feature window resident
+compulsory = n * F * 4 * 2 + nnz * 8 + (n + 1) * 8
+gather_bytes = nnz * F * 4
+if os.environ.get("PROP_ONE_HOP"):  # ncu: one hop into the loader store, nothing else
+    deg = torch.diff(row_ptr).to(torch.int32)
+    L = pp.Loader(data=X, where=pp.PP_MEM_DEVICE, num_nodes=n, num_hops=2, feat_dim=F, hop_stride=0, row_stride=F,
+                  dtype=pp.PP_F32, batch_size=8192, out_dtype=pp.PP_BF16)
+    L.propagate_store(1, row_ptr, col, deg, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    L.close()
+    sys.exit(0)
 hops = torch.empty((K + 1, n, F), device="cuda")
 torch.cuda.synchronize()
 pp.pp_propagate(row_ptr, col, X, K, hops)  # warm-up
@@ -51,7 +64,10 @@ total = K * per_hop + nnz * (8 + 8 + 16) + 2 * n * F * 4
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 print(json.dumps({"config": "products-sized ER graph", "n": n, "nnz": nnz, "F": F, "K": K, "ms": ms,
                   "algorithmic_GBs": total / ms / 1e6, "frac_hbm": total / ms / 1e6 / peak,
-                  "ms_per_hop": ms / K}))
+                  "ms_per_hop": ms / K, "compulsory_bytes_per_hop": compulsory,
+                  "compulsory_GBs": compulsory * K / ms / 1e6, "gather_bytes_per_hop": gather_bytes,
+                  "gather_GBs": gather_bytes * K / ms / 1e6,
+                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (sliced above 64 MB per hop)")}))
 
 # Same graph, propagated INTO a loader store (pp_propagate_store: node-major [n, K+1, F] fp32
 # records, hop slot k from slot k-1, weights from the degree array on the fly).
@@ -76,7 +92,9 @@ b.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
 per_hop = nnz * (F * 4 + 8 + 4) + n * (F * 4 + 16)
-print(json.dumps({"config": "products-sized ER graph, into the loader store", "kernel": "k_spmm_store_v4", "n": n,
+print(json.dumps({"config": "products-sized ER graph, into the loader store",
+                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (sliced above 64 MB per hop)"), "n": n,
                   "nnz": nnz, "F": F, "K": K, "ms": ms, "algorithmic_GBs": K * per_hop / ms / 1e6,
+                  "compulsory_GBs": compulsory * K / ms / 1e6, "gather_GBs": gather_bytes * K / ms / 1e6,
                   "frac_hbm": K * per_hop / ms / 1e6 / peak, "ms_per_hop": ms / K}))
 L.close()
