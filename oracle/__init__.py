@@ -287,14 +287,21 @@ def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
     return (np.asarray(bits, dtype=np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
 
 
-def hop_linear(batch_bits: np.ndarray, W_bits: np.ndarray):
+def f16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
+    """binary16 bit patterns -> exact float64 values."""
+    return np.asarray(bits, dtype=np.uint16).view(np.float16).astype(np.float64)
+
+
+def hop_linear(batch_bits: np.ndarray, W_bits: np.ndarray, dtype: int = BF16):
     """SIGN's per-hop linear layer (one weight matrix per hop) on a batch:
-    Z[j, k, :] = X[j, k, :] @ W[k] in float64 from the exact bf16 values (numpy matmul as the
-    library step).  batch_bits: bf16 bits [rows, H, F] (the oracle batch, O10); W_bits: bf16 bits
-    [H, F, D].  Returns (Z, S) with S[j, k, :] = |X[j, k, :]| @ |W[k]| (the scale of the
-    rounding-error bound of any summation order)."""
-    X = bf16_bits_to_f64(batch_bits)
-    Wf = bf16_bits_to_f64(W_bits)
+    Z[j, k, :] = X[j, k, :] @ W[k] in float64 from the exact 16-bit values (numpy matmul as the
+    library step).  batch_bits: bf16 (dtype BF16) or binary16 (dtype F16) bits [rows, H, F] (the
+    oracle batch, O10); W_bits: the same type's bits [H, F, D].  Returns (Z, S) with
+    S[j, k, :] = |X[j, k, :]| @ |W[k]| (the scale of the rounding-error bound of any summation
+    order)."""
+    to64 = bf16_bits_to_f64 if dtype == BF16 else f16_bits_to_f64
+    X = to64(batch_bits)
+    Wf = to64(W_bits)
     Z = np.einsum("jkf,kfd->jkd", X, Wf)
     S = np.einsum("jkf,kfd->jkd", np.abs(X), np.abs(Wf))
     return Z, S

@@ -117,8 +117,15 @@ struct LinearArgs {
   int32_t l2_prefetch;      // 1: bulk L2 prefetch of the next tile's rows (PPLOAD_LINEAR_PREFETCH, default 1)
   int32_t z_tma;            // set by launch_gather_linear: Z tensor map encoded, epilogue uses TMA stores
   uint64_t* ts;             // experiment probe (PPLOAD_DEBUG_TS): per-tile timestamps of CTA 0, or null
+  // K-chunked kernel (any F % 8 == 0; any store dtype; spilled / sharded stores)
+  int32_t in_dtype = 0, out_dtype = 1;  // store dtype; A operand = W dtype = out_dtype (bf16 / f16)
+  int32_t world = 1;                    // owners: row v on shards[v % world] at local row v / world
+  ShardView shards[kMaxWorld];
 };
 bool linear_supported(int H, int F, int D, int num_sms);
+// The K-chunked kernel: F % 8 == 0, D in {256, 512}, 16-bit batch dtype.
+bool linear_kc_supported(int H, int F, int D, int num_sms, int out_dtype);
+cudaError_t launch_gather_linear_kc(const LinearArgs& a, bool pdl, cudaStream_t st);
 // Encodes the Z and W tensor maps and launches the fused kernel on `st`.
 // pdl: programmatic dependent launch (only right after another fused launch of this
 // epoch on `st`: launches are independent, so the next grid's CTAs may start on SMs

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -613,6 +614,439 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, bool pdl, cudaStream_t 
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_gather_linear, a, zmap, wmap);
+}
+
+
+// ==== K-chunked variant: any F (% 8), 16-bit batch dtype, spilled / sharded stores ==============
+// The F <= 128 kernel above keeps all of W_k resident; with F = 768 (MAG240M) or 1024 (IGB-large)
+// W_k is 0.75-1 MB, so here the reduction dimension is walked in chunks of 64: per 128-row M-tile
+// and chunk, the producers write a 16 KB A chunk (128 rows x 64 elements, K-major SWIZZLE_128B) and
+// a loader warp brings the matching 64 x D slice of W_k by TMA (D / 64 boxes of 64 x 64, MN-major
+// SWIZZLE_128B; rows >= F zero-filled).  4 A stages, 2 W stages, the same TMEM accumulators and
+// TMA-store epilogue as above.  W_k is re-read from L2 for every tile (it is the same for all of a
+// CTA's tiles), F x D x 2 bytes per 128 rows.
+//   A operand = the batch the loader would produce: fp32 records cast with cvt.rn to bf16 / f16,
+//   16-bit records copied; W (and the MMA's input kind) in that same 16-bit type.
+//   Rows resolve through the shard views (owner v mod W, HBM / pinned spill / peer HBM), so spilled
+//   and sharded stores work; peer rows are read as store records (not the exchange copy).
+namespace {
+constexpr int kKcChunk = 64;                     // K elements per chunk (one 128-B swizzle row of bf16)
+constexpr int kKcAStages = 4;
+constexpr int kKcWStages = 2;
+constexpr int kKcABytes = kTileM * 128;          // 16 KB: 128 rows x 64 bf16
+constexpr int kKcWBox = kKcChunk * 128;          // 8 KB: 64 K rows x 64 columns
+constexpr int kKcWMaxBytes = (512 / 64) * kKcWBox;  // 64 KB per W stage at D = 512
+constexpr int kKcLoaderWarp = 9;
+
+__device__ __forceinline__ uint64_t kc_w_desc(const void* p) {  // MN-major SW128, LBO = 8 KB between boxes
+  return static_cast<uint64_t>((smem_addr(p) >> 4) & 0x3FFFu) | (static_cast<uint64_t>(kKcWBox >> 4) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ uint32_t kc_idesc(int out_dtype) {
+  const uint32_t fmt = out_dtype == 2 ? 0u : 1u;  // kind::f16 operand format: 0 = F16, 1 = BF16
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | (static_cast<uint32_t>(kUmmaN >> 3) << 17) |
+         (static_cast<uint32_t>(kTileM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t f16x2(uint32_t lo, uint32_t hi) {
+  const __half2 h = __floats2half2_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kLinThreads, 1)
+    k_gather_linear_kc(const LinearArgs a, const __grid_constant__ CUtensorMap zmap,
+                       const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ uint8_t smem_raw[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int D = a.D;
+  const int w_stage_bytes = (D / 64) * kKcWBox;
+  uint8_t* w_s = smem;                                    // [kKcWStages][D / 64 boxes][64 K rows][128 B]
+  uint8_t* a_s = w_s + kKcWStages * w_stage_bytes;        // [kKcAStages][128 rows][128 B]
+  uint8_t* z_s = a_s + kKcAStages * kKcABytes;            // epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * kEpiBufs * kStageBytes);
+  uint64_t* a_full = bars;                                // [kKcAStages]
+  uint64_t* a_empty = a_full + kKcAStages;                // [kKcAStages]
+  uint64_t* w_full = a_empty + kKcAStages;                // [kKcWStages]
+  uint64_t* w_empty = w_full + kKcWStages;                // [kKcWStages]
+  uint64_t* t_full = w_empty + kKcWStages;                // [2]
+  uint64_t* t_empty = t_full + 2;                         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = a.H, F = a.F;
+  const int k = blockIdx.x % H;
+  const int q = blockIdx.x / H, Q = gridDim.x / H;
+  const int nh = D / kUmmaN;
+  const int nch = (F + kKcChunk - 1) / kKcChunk;
+  const int s_in = a.in_dtype == 0 ? 4 : 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kKcAStages; ++s) {
+      bar_init(&a_full[s], kProducerThreads);
+      bar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kKcWStages; ++s) {
+      bar_init(&w_full[s], 1);
+      bar_init(&w_empty[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      bar_init(&t_full[h], 1);
+      uint32_t cnt = 0;
+      for (int g = 0; g < kEpiGroups; ++g) {
+        const int lo = g * D / kEpiGroups, hi = (g + 1) * D / kEpiGroups;
+        if (lo < (h + 1) * kUmmaN && hi > h * kUmmaN) cnt += 128;
+      }
+      bar_init(&t_empty[h], cnt > 0 ? cnt : 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t tiles_per_step = (a.B + kTileM - 1) / kTileM;
+  const int64_t total = tiles_per_step * a.nsteps;
+  auto tile_rows = [&](int64_t t, int64_t& step, int& r0, int64_t& pos) -> int {
+    step = t / tiles_per_step;
+    r0 = static_cast<int>(t - step * tiles_per_step) * kTileM;
+    pos = a.first_pos + step * a.step_stride;
+    const int64_t nrows = min(static_cast<int64_t>(a.B), a.N - pos);
+    return static_cast<int>(min(static_cast<int64_t>(kTileM), nrows - r0));
+  };
+  auto next_tile = [&](int64_t t) -> int64_t {
+    for (; t < total; t += Q) {
+      int64_t st_, ps_;
+      int r_;
+      if (tile_rows(t, st_, r_, ps_) > 0) return t;
+    }
+    return total;
+  };
+
+  if (warp < kProducerWarps) {
+    // ---------------- producers: warp w owns rows 16w..16w+15 of every tile.  Lanes 0-15 resolve
+    // the 16 row pointers once per tile; per chunk, fp32 records: half-warp per row (lane c loads
+    // elements 4c..4c+3 of the chunk, 16 B), 8 iterations; 16-bit records: quarter-warp per row
+    // (lane c8 loads elements 8 c8..8 c8+7), 4 iterations.  The next chunk's loads are issued before
+    // the current chunk is converted and stored.
+    const int rbase = warp * 16;
+    constexpr uint32_t kNoRow = 0xffffffffu;
+    auto fetch_index = [&](int64_t t) -> uint32_t {
+      if (t >= total) return kNoRow;
+      int64_t step, pos;
+      int r0;
+      const int rows = tile_rows(t, step, r0, pos);
+      uint32_t v = kNoRow;
+      if (lane < 16 && rbase + lane < rows)
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a.order + pos + r0 + rbase + lane));
+      return v;
+    };
+    auto resolve = [&](uint32_t idx) -> const uint8_t* {  // this lane's row record (hop k), or null
+      if (idx == kNoRow) return nullptr;
+      uint64_t v = idx;
+      if (a.node_set != nullptr) v = static_cast<uint64_t>(a.node_set[v]);
+      const uint64_t W = static_cast<uint64_t>(a.world);
+      const ShardView sh = a.shards[W > 1 ? v % W : 0];
+      const int64_t l = static_cast<int64_t>(W > 1 ? v / W : v);
+      const uint8_t* rec = l < sh.n_hbm ? sh.hbm + l * a.rec_stride : sh.spill + (l - sh.n_hbm) * a.rec_stride;
+      return rec + static_cast<int64_t>(k) * F * s_in;
+    };
+    const bool f32 = s_in == 4;
+    const int hw = lane >> 4, c16 = lane & 15;  // fp32 records
+    const int qw = lane >> 3, c8 = lane & 7;    // 16-bit records
+    auto load_chunk = [&](const uint8_t* my_src, int ch, uint4 (&x)[8]) {
+      if (f32) {
+        const int e = ch * kKcChunk + 4 * c16;  // first element of this lane's 16 B
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const uint8_t* src =
+              reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_src), 2 * it + hw));
+          x[it] = (src != nullptr && e < F && !(a.debug & 1)) ? ldg16(src + static_cast<int64_t>(e) * 4)
+                                                             : make_uint4(0, 0, 0, 0);
+        }
+      } else {
+        const int e = ch * kKcChunk + 8 * c8;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const uint8_t* src =
+              reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_src), 4 * it + qw));
+          x[it] = (src != nullptr && e < F && !(a.debug & 1)) ? ldg16(src + static_cast<int64_t>(e) * 2)
+                                                             : make_uint4(0, 0, 0, 0);
+        }
+      }
+    };
+    auto store_chunk = [&](int64_t u, const uint4 (&x)[8]) {
+      const int s = static_cast<int>(u % kKcAStages);
+      bar_wait(&a_empty[s], (static_cast<uint32_t>(u / kKcAStages) & 1u) ^ 1u);
+      uint8_t* at = a_s + s * kKcABytes;
+      if (f32) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = rbase + 2 * it + hw;
+          const uint32_t off = sw128(r, c16 >> 1) + (c16 & 1) * 8;
+          const uint4 v = x[it];
+          *reinterpret_cast<uint2*>(at + off) =
+              a.out_dtype == 2 ? make_uint2(f16x2(v.x, v.y), f16x2(v.z, v.w)) : make_uint2(bf16x2(v.x, v.y), bf16x2(v.z, v.w));
+        }
+      } else {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int r = rbase + 4 * it + qw;
+          *reinterpret_cast<uint4*>(at + sw128(r, c8)) = x[it];
+        }
+      }
+      fence_async_smem();
+      bar_arrive(&a_full[s]);
+    };
+    // Register-staged loads keep only two chunks (64 KB per SM) in flight, less than HBM latency
+    // needs, so each lane also pulls its row's chunk pf chunks ahead into L2 with one bulk prefetch
+    // (no registers): the loads then hit L2.  Crossing into the next tile uses its rows.
+    const int pf = a.l2_prefetch > 0 ? a.l2_prefetch : 0;
+    const int chunk_bytes = kKcChunk * s_in;
+    auto prefetch_chunk = [&](const uint8_t* my_src, int ch) {
+      if (lane < 16 && my_src != nullptr && ch * kKcChunk < F) {
+        const int bytes = min(chunk_bytes, (F - ch * kKcChunk) * s_in);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(my_src + static_cast<int64_t>(ch) * chunk_bytes),
+                     "r"(bytes)
+                     : "memory");
+      }
+    };
+    uint4 xa[8], xb[8];
+    int64_t u = 0;  // unit counter: (tile, chunk) pairs in order
+    int64_t t = next_tile(q);
+    const uint8_t* src = t < total ? resolve(fetch_index(t)) : nullptr;
+    int64_t t_next = t < total ? next_tile(t + Q) : total;
+    const uint8_t* src_next = t_next < total ? resolve(fetch_index(t_next)) : nullptr;
+    for (int d = 0; d < pf; ++d) prefetch_chunk(d < nch ? src : src_next, d < nch ? d : d - nch);
+    while (t < total) {
+      load_chunk(src, 0, xa);
+      for (int ch = 0; ch < nch; ++ch) {
+        const int p = ch + pf;  // the unit pf ahead: this tile or the next one
+        if (pf > 0) prefetch_chunk(p < nch ? src : src_next, p < nch ? p : p - nch);
+        // issue chunk ch + 1 before storing chunk ch (the two register buffers alternate)
+        if (ch % 2 == 0) {
+          if (ch + 1 < nch) load_chunk(src, ch + 1, xb);
+          store_chunk(u++, xa);
+        } else {
+          if (ch + 1 < nch) load_chunk(src, ch + 1, xa);
+          store_chunk(u++, xb);
+        }
+      }
+      t = t_next;
+      src = src_next;
+      t_next = t < total ? next_tile(t + Q) : total;
+      src_next = t_next < total ? resolve(fetch_index(t_next)) : nullptr;
+    }
+  } else if (warp == kKcLoaderWarp) {
+    // ---------------- W loader: the same (tile, chunk) sequence; chunk ch of W_k into stage u % 2
+    if (lane == 0) {
+      const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
+      const uint32_t nbox = static_cast<uint32_t>(D / 64);
+      int64_t u = 0;
+      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+        for (int ch = 0; ch < nch; ++ch, ++u) {
+          const int s = static_cast<int>(u % kKcWStages);
+          bar_wait(&w_empty[s], (static_cast<uint32_t>(u / kKcWStages) & 1u) ^ 1u);
+          if (a.debug & 16) {  // experiment: no W traffic (the MMAs read stale shared memory)
+            bar_arrive(&w_full[s]);
+            continue;
+          }
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&w_full[s])),
+                       "r"(nbox * kKcWBox)
+                       : "memory");
+          for (uint32_t b = 0; b < nbox; ++b)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];" ::"r"(smem_addr(w_s + s * w_stage_bytes + b * kKcWBox)),
+                "l"(wmap_addr), "r"(static_cast<int>(b * 64)), "r"(ch * kKcChunk), "r"(k), "r"(smem_addr(&w_full[s]))
+                : "memory");
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer: per unit, 4 K-steps of 16 into each accumulator
+    if (lane == 0) {
+      const uint32_t idesc = kc_idesc(a.out_dtype);
+      int64_t u = 0;
+      int i = 0;
+      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
+        for (int ch = 0; ch < nch; ++ch, ++u) {
+          const int sa = static_cast<int>(u % kKcAStages), sw = static_cast<int>(u % kKcWStages);
+          if (ch == 0)
+            for (int h = 0; h < nh; ++h) bar_wait(&t_empty[h], (i & 1) ^ 1);
+          bar_wait(&a_full[sa], static_cast<uint32_t>(u / kKcAStages) & 1u);
+          bar_wait(&w_full[sw], static_cast<uint32_t>(u / kKcWStages) & 1u);
+          tc_fence_after();
+          const uint8_t* at = a_s + sa * kKcABytes;
+          const uint8_t* wt = w_s + sw * w_stage_bytes;
+          for (int h = 0; h < ((a.debug & 64) ? 0 : nh); ++h) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint64_t ad = sw128_desc(at) + 2 * j;                             // +32 B per 16 K
+              const uint64_t bd = kc_w_desc(wt + h * (kUmmaN / 64) * kKcWBox + j * 2048);  // 16 K rows per step
+              umma_i(tmem + h * kUmmaN, ad, bd, idesc, (ch > 0 || j > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&a_empty[sa]);
+          umma_commit(&w_empty[sw]);
+          if (ch == nch - 1)
+            for (int h = 0; h < nh; ++h) umma_commit(&t_full[h]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue (as in k_gather_linear)
+    const int e = warp & 3;
+    const int grp = (warp - kEpiWarp0) >> 2;
+    uint8_t* sbuf = z_s + (warp - kEpiWarp0) * kEpiBufs * kStageBytes;
+    const int cols_per_slice = 128 / a.z_elem;
+    const uint64_t zmap_addr = reinterpret_cast<uint64_t>(&zmap);
+    int i = 0, slice = 0;
+    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
+      int64_t step, pos;
+      int r0;
+      const int rows = tile_rows(t, step, r0, pos);
+      const bool tma_rows = a.z_tma && e * 32 + 32 <= rows;
+      for (int h = 0; h < nh; ++h) {
+        const int c_lo = max(grp * D / kEpiGroups, h * kUmmaN) - h * kUmmaN;
+        const int c_hi = min((grp + 1) * D / kEpiGroups, (h + 1) * kUmmaN) - h * kUmmaN;
+        if (c_lo >= c_hi) continue;
+        bar_wait(&t_full[h], i & 1);
+        tc_fence_after();
+        const uint32_t trow = tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN;
+        uint32_t v[64];
+        auto ld_slice = [&](int c0) {
+          PPL_TMEM_LD32(trow + c0, v);
+          if (a.z_elem == 2) PPL_TMEM_LD32(trow + c0 + 32, (v + 32));
+        };
+        ld_slice(c_lo);
+#pragma unroll 1
+        for (int c0 = c_lo; c0 < c_hi; c0 += cols_per_slice) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
+          __syncwarp();
+          uint8_t* sb = sbuf + (slice % kEpiBufs) * kStageBytes;
+          ++slice;
+          uint8_t* my = sb + lane * 128;
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (a.z_elem == 2) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                             bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          if (c0 + cols_per_slice < c_hi) ld_slice(c0 + cols_per_slice);
+          __syncwarp();
+          if (a.debug & 2) continue;  // experiment: no Z stores
+          if (tma_rows) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(zmap_addr),
+                  "r"(h * kUmmaN + c0), "r"(k), "r"(r0 + e * 32), "r"(static_cast<int>(step)), "r"(smem_addr(sb))
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          } else {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int rr = it * 4 + (lane >> 3), chk = lane & 7;
+              const uint4 y = *reinterpret_cast<const uint4*>(sb + rr * 128 + ((chk ^ (rr & 7)) << 4));
+              if (e * 32 + rr < rows) {
+                uint8_t* d = a.Z + step * a.z_stride +
+                             ((static_cast<int64_t>(r0 + e * 32 + rr) * H + k) * D + h * kUmmaN + c0) * a.z_elem +
+                             chk * 16;
+                *reinterpret_cast<uint4*>(d) = y;
+              }
+            }
+            __syncwarp();
+          }
+        }
+        tc_fence_before();
+        bar_arrive(&t_empty[h]);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+static size_t linear_kc_smem_bytes(int D) {
+  return 1024 + static_cast<size_t>(kKcWStages) * (D / 64) * kKcWBox + kKcAStages * kKcABytes +
+         kEpiWarps * kEpiBufs * kStageBytes + 256;
+}
+
+bool linear_kc_supported(int H, int F, int D, int num_sms, int out_dtype) {
+  return F >= 8 && F % 8 == 0 && (D == 256 || D == 512) && H >= 1 && H <= num_sms && (out_dtype == 1 || out_dtype == 2);
+}
+
+namespace {
+// W as {column d, row f, hop k} of the batch dtype, box 64 columns x 64 rows (one K chunk).
+bool encode_w_map_kc(const LinearArgs& a, CUtensorMap* m) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (encode == nullptr) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.F), static_cast<cuuint64_t>(a.H)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.D) * 2, static_cast<cuuint64_t>(a.F) * a.D * 2};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kKcChunk), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(m, a.out_dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                const_cast<void*>(a.W), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream_t st) {
+  if (!linear_kc_supported(a_in.H, a_in.F, a_in.D, a_in.num_sms, a_in.out_dtype)) return cudaErrorInvalidValue;
+  const size_t smem = linear_kc_smem_bytes(a_in.D);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gather_linear_kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(linear_kc_smem_bytes(512)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  LinearArgs a = a_in;
+  alignas(64) CUtensorMap zmap{};
+  a.z_tma = encode_z_map(a, &zmap) ? 1 : 0;
+  alignas(64) CUtensorMap wmap{};
+  if (!encode_w_map_kc(a, &wmap)) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
+  cfg.blockDim = dim3(kLinThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  lattr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gather_linear_kc, a, zmap, wmap);
 }
 
 }  // namespace ppl

@@ -1413,11 +1413,16 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1 || !W || !Z) return fail(PP_ERR_INVALID, "NULL argument or n < 1");
-  if (L->in_dtype != PP_F32 || L->n_spill > 0 || L->W != 1 || L->files)
-    return fail(PP_ERR_INVALID, "fused linear needs an fp32, HBM-resident, unsharded store");
-  if (!linear_supported(L->H, L->F, D, L->num_sms))
-    return fail(PP_ERR_INVALID, "fused linear supports F <= 128 with F %% 4 == 0 and D in {256, 512} (F=%d, D=%d)",
-                L->F, D);
+  if (L->files) return fail(PP_ERR_INVALID, "fused linear needs an in-memory store (not the storage tier)");
+  if (L->out_dtype == PP_F32) return fail(PP_ERR_INVALID, "fused linear needs a 16-bit batch dtype (bf16 / f16)");
+  // the F <= 128 kernel (W_k resident in shared memory) for fp32 -> bf16 unsharded HBM stores; the
+  // K-chunked kernel for every other shape, dtype and placement
+  const char* kc_env = getenv("PPLOAD_LINEAR");
+  const bool resident = L->in_dtype == PP_F32 && L->out_dtype == PP_BF16 && L->n_spill == 0 && L->W == 1 &&
+                        linear_supported(L->H, L->F, D, L->num_sms) && !(kc_env && !strcmp(kc_env, "kc"));
+  if (!resident && !linear_kc_supported(L->H, L->F, D, L->num_sms, L->out_dtype))
+    return fail(PP_ERR_INVALID, "fused linear supports F %% 8 == 0 (F %% 4 == 0 when F <= 128) and D in {256, 512} "
+                "(F=%d, D=%d)", L->F, D);
   if (z_dtype != PP_BF16 && z_dtype != PP_F32) return fail(PP_ERR_INVALID, "z_dtype must be PP_BF16 or PP_F32");
   if (reinterpret_cast<uintptr_t>(W) % 16 || reinterpret_cast<uintptr_t>(Z) % 16 || z_stride_bytes % 16)
     return fail(PP_ERR_INVALID, "W, Z and z_stride_bytes must be 16-byte aligned");
@@ -1425,6 +1430,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   if (n > 1 && z_stride_bytes < L->B * L->H * static_cast<int64_t>(D) * z_elem)
     return fail(PP_ERR_INVALID, "z_stride_bytes smaller than one step");
   if (!L->permuted) return fail(PP_ERR_STATE, "pp_next_batches_linear before pp_epoch_permute");
+  if (!L->linked && !L->local) return fail(PP_ERR_STATE, "sharded loader: peers not linked yet");
   if (L->cursor >= L->steps) {
     rows[0] = 0;
     if (n_done) *n_done = 0;
@@ -1443,9 +1449,10 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.node_set = L->compact ? nullptr : L->d_node_set;
   a.store = L->d_store;
   a.rec_stride = L->rec_stride;
-  a.N = L->N;
-  a.first_pos = L->cursor * L->B;
-  a.step_stride = L->B;
+  // step t of this rank: positions [tWB + rB, ...) of the global order, or [tB, ...) of a local epoch
+  a.N = L->local ? L->local_rows : L->N;
+  a.first_pos = L->local ? L->cursor * L->B : L->cursor * L->B * L->W + static_cast<int64_t>(L->rank) * L->B;
+  a.step_stride = L->local ? L->B : L->B * L->W;
   a.B = static_cast<int32_t>(L->B);
   a.nsteps = static_cast<int32_t>(nsteps);
   a.W = W;
@@ -1456,11 +1463,15 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.z_stride = z_stride_bytes;
   a.z_elem = z_elem;
   a.num_sms = L->num_sms;
+  a.in_dtype = L->in_dtype;
+  a.out_dtype = L->out_dtype;
+  a.world = L->W;
+  for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = ShardView{L->shards[i].hbm, L->shards[i].spill, L->shards[i].n_hbm};
   if (const char* e = getenv("PPLOAD_DEBUG_LINEAR")) a.debug = atoi(e);
-  a.l2_prefetch = 1;
+  a.l2_prefetch = resident ? 1 : 4;  // resident kernel: next tile's rows; K-chunked: chunks ahead
   if (const char* e = getenv("PPLOAD_LINEAR_PREFETCH")) a.l2_prefetch = atoi(e);
   static uint64_t* dbg_ts = nullptr;  // experiment probe: timestamps of CTA 0 (PPLOAD_DEBUG_TS=1)
-  const bool want_ts = getenv("PPLOAD_DEBUG_TS") != nullptr;
+  const bool want_ts = resident && getenv("PPLOAD_DEBUG_TS") != nullptr;
   if (want_ts && !dbg_ts) PPL_CUDA(L, cudaMalloc(&dbg_ts, (24 * 14 + 4 * 1024) * 8));
   if (want_ts) {
     PPL_CUDA(L, cudaMemsetAsync(dbg_ts, 0, (24 * 14 + 4 * 1024) * 8, L->stream));
@@ -1470,7 +1481,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   zspans[0].lo = reinterpret_cast<uintptr_t>(Z);
   zspans[0].hi = zspans[0].lo + static_cast<uintptr_t>((nsteps - 1) * z_stride_bytes + L->B * L->H * D * z_elem);
   const bool pdl = !handoff && chain_pdl(L, pp_loader::kLastLinear, zspans);
-  PPL_CUDA(L, launch_gather_linear(a, pdl, L->stream));
+  PPL_CUDA(L, resident ? launch_gather_linear(a, pdl, L->stream) : launch_gather_linear_kc(a, pdl, L->stream));
   L->pdl_launches += pdl ? 1 : 0;
   if (want_ts) {
     static uint64_t h[24 * 14 + 4 * 1024];
@@ -1503,7 +1514,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
     PPL_CUDA(L, cudaStreamWaitEvent(cons, L->ev_out, 0));
   }
   for (int64_t i = 0; i < nsteps; ++i)
-    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, L->N - (L->cursor + i) * L->B)));
+    rows[i] = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(L->B, a.N - (a.first_pos + i * a.step_stride))));
   L->cursor += nsteps;
   if (n_done) *n_done = static_cast<int32_t>(nsteps);
   return PP_OK;

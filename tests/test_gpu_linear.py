@@ -109,10 +109,16 @@ def test_fused_linear_rejects_unsupported(pp):
         assert ei.value.status == pp.PP_ERR_INVALID
     X, hs, rs = hop_tensor(65, H, N, 8)
     with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=8, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
-                   batch_size=64, out_dtype=pp.PP_BF16, hbm_budget_bytes=-1) as L:
+                   batch_size=64, out_dtype=pp.PP_F32) as L:
         L.epoch_permute(1, 1)
         with pytest.raises(pp.PPError) as ei:
-            L.next_batches_linear(1, W, 256, Z, "bf16", 0)  # spilled store
+            L.next_batches_linear(1, W, 256, Z, "bf16", 0)  # fp32 batches: no 16-bit A operand
+        assert ei.value.status == pp.PP_ERR_INVALID
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=8, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=64, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(1, 1)
+        with pytest.raises(pp.PPError) as ei:
+            L.next_batches_linear(1, W, 384, Z, "bf16", 0)  # D not in {256, 512}
         assert ei.value.status == pp.PP_ERR_INVALID
 
 

@@ -1,0 +1,159 @@
+"""§8(f)-1 consumer at every BASELINE row shape: the K-chunked fused gather + per-hop linear
+(k_gather_linear_kc) -- F walked in chunks of 64 with W_k streamed by TMA per chunk, so F = 768
+(MAG240M, fp16 store) and F = 1024 (IGB-large) work, as do spilled, sharded and compact stores.
+Z[j, k, :] = X_k[v_j, :] @ W_k with X in the batch dtype (the O10 batch: bf16 / f16 cast of fp32
+records, or the 16-bit records themselves) and W in that dtype ("learns R+1 weight matrices for each
+hop"; hidden 512).  Checked against oracle.hop_linear (float64) with
+the tolerance of tests/test_gpu_linear.py at K = F rounded up to the chunk: 16-bit products are exact
+in fp32, then K - 1 fp32 additions (2 K 2^-24 sum|x w| allowed) and, for bf16 Z, one RNE rounding."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import hop_tensor, node_set as make_node_set
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TDT = {oracle.BF16: torch.bfloat16, oracle.F16: torch.float16}
+
+
+@pytest.fixture(scope="module")
+def pp():
+    import __graft_entry__ as ge
+
+    ge.build()
+    import paper_2504_13266_b200 as pp
+
+    return pp
+
+
+def weights(seed, H, F, D, dt):
+    rng = np.random.default_rng(seed)
+    w = (rng.standard_normal((H, F, D)) / np.sqrt(F)).astype(np.float32).view(np.uint32)
+    return oracle.cast_bf16(w) if dt == oracle.BF16 else oracle.cast_f16(w)
+
+
+def check(Zgpu, zdt, batch_bits, wbits, dt, F):
+    Zref, S = oracle.hop_linear(batch_bits, wbits, dt)
+    K = -(-F // 64) * 64
+    tol = 2 * K * 2.0 ** -24 * S
+    if zdt == "bf16":
+        got = oracle.bf16_bits_to_f64(Zgpu.view(torch.int16).cpu().numpy().view(np.uint16))
+        tol = tol + 2.0 ** -8 * np.abs(Zref)
+    else:
+        got = Zgpu.cpu().numpy().astype(np.float64)
+    err = np.abs(got - Zref)
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} of {bad.size} outside tolerance; worst excess {(err - tol).max()}"
+
+
+def run_and_check(pp, L, bits, in_dt, hs, rs, H, F, D, order, B, out_dt, zdt, W=1, r=0, k=2, seed=70):
+    wb = weights(seed, H, F, D, out_dt)
+    Wd = torch.from_numpy(wb.view(np.int16).copy()).cuda().view(TDT[out_dt])
+    tdt = torch.bfloat16 if zdt == "bf16" else torch.float32
+    esz = 2 if zdt == "bf16" else 4
+    steps = oracle.num_steps(order.shape[0], B, W)
+    Z = torch.empty((k, B, H, D), dtype=tdt, device="cuda")
+    t = 0
+    while t < steps:
+        Z.fill_(float("nan"))
+        rows = L.next_batches_linear(k, Wd, D, Z, zdt, B * H * D * esz)
+        torch.cuda.synchronize()
+        for i, nr in enumerate(rows):
+            want, _, _ = oracle.batch(bits, in_dt, hs, rs, H, F, order, B, W, t + i, r, out_dt)
+            assert nr == want.shape[0]
+            if nr:
+                check(Z[i, :nr], zdt, want, wb, out_dt, F)
+            if nr < B:
+                assert torch.isnan(Z[i, nr:].float()).all()
+        t += len(rows)
+
+
+@pytest.mark.parametrize("F,D,out_dt,zdt", [(1024, 512, oracle.BF16, "bf16"), (768, 256, oracle.F16, "f32"),
+                                            (136, 512, oracle.BF16, "f32"), (8, 256, oracle.F16, "bf16"),
+                                            (200, 512, oracle.F16, "bf16")])
+def test_kc_fp32_store(pp, F, D, out_dt, zdt):
+    H, N, B = 3, 1500, 256
+    X, hs, rs = hop_tensor(71 + F, H, N, F)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=out_dt) as L:
+        L.epoch_permute(4, 1)
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, oracle.epoch_order(4, N, 1), B, out_dt, zdt)
+
+
+@pytest.mark.parametrize("dt", [oracle.F16, oracle.BF16])
+def test_kc_sixteen_bit_store_mag240m_rows(pp, dt):
+    # configs[4] row shape: fp16 records of 4 x 768 copied into the A operand as they are
+    H, N, F, B, D = 4, 1200, 768, 512, 512
+    X, hs, rs = hop_tensor(72, H, N, F, dtype=np.uint16)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=dt,
+                   batch_size=B, out_dtype=dt) as L:
+        L.epoch_permute(5, 8)
+        run_and_check(pp, L, X, dt, hs, rs, H, F, D, oracle.epoch_order(5, N, 8), B, dt, "f32")
+
+
+def test_kc_spilled_compact_store(pp):
+    H, N, F, B, D = 3, 3000, 96, 200, 256
+    X, hs, rs = hop_tensor(73, H, N, F)
+    S = make_node_set(74, N, 2100)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   node_set=S, store_set_only=True, batch_size=B, out_dtype=pp.PP_BF16,
+                   hbm_budget_bytes=700 * H * F * 4) as L:
+        assert L.query()["rows_spill"] > 0
+        L.epoch_permute(6, 16)
+        order = oracle.epoch_order(6, S.shape[0], 16, node_set=S)
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "bf16")
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_kc_sharded_loopback(pp, W):
+    # every rank's batches (global permutation, slice r of each step) with rows read from the owners
+    H, N, F, B, D = 2, 2500, 128, 160, 512
+    X, hs, rs = hop_tensor(75, H, N, F)
+    Ls = [pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                    batch_size=B, out_dtype=pp.PP_BF16, world_size=W, rank=r, peers=pp.PP_PEERS_LOOPBACK)
+          for r in range(W)]
+    pp.pp_link_loopback([L.h for L in Ls])
+    try:
+        order = oracle.epoch_order(7, N, 4)
+        for r, L in enumerate(Ls):
+            L.epoch_permute(7, 4)
+            run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "f32",
+                          W=W, r=r)
+    finally:
+        for L in Ls:
+            L.close()
+
+
+def test_kc_equals_resident_kernel(pp, monkeypatch):
+    # F = 128 runs on the resident-W kernel by default; PPLOAD_LINEAR=kc forces the K-chunked one.
+    # Both accumulate the same exact products in fp32 (orders may differ): each within tolerance
+    H, N, F, B, D = 4, 2000, 128, 512, 512
+    X, hs, rs = hop_tensor(76, H, N, F)
+    for mode in ("", "kc"):
+        monkeypatch.setenv("PPLOAD_LINEAR", mode)
+        with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                       batch_size=B, out_dtype=pp.PP_BF16) as L:
+            L.epoch_permute(8, 1)
+            run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, oracle.epoch_order(8, N, 1), B,
+                          oracle.BF16, "bf16", k=3)
+
+
+def test_kc_local_epoch(pp):
+    # a locality-aware epoch (pp_epoch_permute_local) on a sharded loader: this rank's rows only
+    H, N, F, B, D = 2, 3001, 64, 128, 256
+    X, hs, rs = hop_tensor(77, H, N, F)
+    Ls = [pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                    batch_size=B, out_dtype=pp.PP_BF16, world_size=2, rank=r, peers=pp.PP_PEERS_LOOPBACK)
+          for r in range(2)]
+    pp.pp_link_loopback([L.h for L in Ls])
+    try:
+        L = Ls[1]
+        L.epoch_permute_local(9, 1)
+        local = L.query()["local_rows"]
+        order = oracle.epoch_order(9, local, 1) * 2 + 1
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "f32")
+    finally:
+        for L_ in Ls:
+            L_.close()

@@ -34,3 +34,25 @@ def test_hop_linear_identity_and_hop_separation():
     X = oracle.bf16_bits_to_f64(xb)
     for k, c in enumerate((1.0, -2.0, 0.5)):
         assert np.array_equal(Z[:, k, :], c * X[:, k, :])
+
+
+def test_hop_linear_binary16_brute_force_loops():
+    # the fp16 batch / weights form (fp16 stores, e.g. MAG240M): decoded by IEEE binary16 rules written
+    # out here (sign, 5-bit exponent, 10-bit mantissa, subnormals), summed in Python floats
+    def half(b):
+        b = int(b)
+        s, e, m = b >> 15, (b >> 10) & 31, b & 1023
+        v = (m / 1024.0) * 2.0 ** -14 if e == 0 else (1 + m / 1024.0) * 2.0 ** (e - 15)
+        return -v if s else v
+
+    rng = np.random.default_rng(2)
+    R, H, F, D = 3, 2, 6, 3
+    xb = oracle.cast_f16(rng.standard_normal((R, H, F)).astype(np.float32).view(np.uint32))
+    wb = oracle.cast_f16((rng.standard_normal((H, F, D)) * 1e-4).astype(np.float32).view(np.uint32))  # subnormals
+    Z, S = oracle.hop_linear(xb, wb, oracle.F16)
+    for j in range(R):
+        for k in range(H):
+            for d in range(D):
+                terms = [half(xb[j, k, f]) * half(wb[k, f, d]) for f in range(F)]
+                assert abs(Z[j, k, d] - sum(terms)) <= 1e-15 * max(1e-12, sum(map(abs, terms)))
+                assert abs(S[j, k, d] - sum(map(abs, terms))) <= 1e-15 * max(1e-12, sum(map(abs, terms)))
