@@ -593,8 +593,11 @@ def next_rows_secondary():
         out["propagation"] = {"error": repr(e)[:300]}
     try:
         st = _script_lines("bench_storage.py", {"PP_STORAGE_EPOCHS": "1"}, timeout=300)[-1]
-        out["storage_tier"] = {k: st[k] for k in ("chunk", "storage_mode", "nodes_per_s", "storage_GBs",
-                                                  "seq_read_GBs_measured", "frac_of_seq_read", "sampled_step_bit_exact")}
+        out["storage_tier"] = {k: st.get(k) for k in ("chunk", "storage_mode", "nodes_per_s", "storage_GBs",
+                                                      "seq_read_GBs_range", "frac_of_seq_read",
+                                                      "frac_of_same_request_seq_read", "sampled_step_bit_exact")}
+        out["storage_tier"]["note"] = ("frac_of_seq_read: against the fastest O_DIRECT sequential read of the "
+                                       "same files measured before and after the epochs (virtio disk; rate drifts)")
     except Exception as e:
         out["storage_tier"] = {"error": repr(e)[:300]}
     try:

@@ -75,11 +75,22 @@ def seq_read_gbs(paths, nthreads, block=64 << 20):
 
 
 nthreads = int(os.environ.get("PPLOAD_IO_THREADS", "16"))
-try:  # best of a few (threads, request size) settings
-    peak = max(seq_read_gbs(paths, t, b) for t in (8, 16, 32) for b in (1 << 20, 8 << 20))
-except OSError as e:
-    peak = None
-    print(json.dumps({"note": f"O_DIRECT sequential read failed: {e}"}), flush=True)
+piece = int(os.environ.get("PPLOAD_IO_PIECE", str(1 << 20)))
+SETTINGS = [(t, b) for t in (8, 16, 32) for b in (1 << 20, 8 << 20)]
+
+
+def seq_rates():
+    """O_DIRECT sequential reads of the same files at each (threads, request size): the disk's rate now.
+    The box's disk is a virtio block device whose rate drifts, so this runs before and after the
+    epochs and the report gives the range."""
+    try:
+        return {f"{t}x{b >> 20}MiB": seq_read_gbs(paths, t, b) for t, b in SETTINGS}
+    except OSError as e:
+        print(json.dumps({"note": f"O_DIRECT sequential read failed: {e}"}), flush=True)
+        return {}
+
+
+seq_before = seq_rates()
 
 L = pp.Loader(files=paths, num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B,
               out_dtype=pp.PP_BF16)
@@ -104,6 +115,11 @@ for e in range(reps):
     epoch(250413267 + e)
 dt = (time.time() - ts) / reps
 nbytes = (L.query()["storage_bytes_read"] - b0) / reps
+seq_after = seq_rates()
+all_rates = list(seq_before.values()) + list(seq_after.values())
+peak = max(all_rates) if all_rates else None
+same_key = f"{nthreads}x{piece >> 20}MiB"  # the loader's own thread count and request size
+same = [r[same_key] for r in (seq_before, seq_after) if same_key in r]
 # parity on a sampled step of the last epoch (numpy reads of the same files)
 L.epoch_permute(999, chunk)
 L.seek(17)
@@ -121,5 +137,9 @@ print(json.dumps({"config": "products-shaped hop files", "N": N, "F": F, "H": H,
                   "epoch_s": dt, "nodes_per_s": N / dt, "storage_GBs": nbytes / dt / 1e9,
                   "bytes_per_epoch": nbytes, "algorithmic_bytes_per_epoch": N * H * F * 4,
                   "seq_read_GBs_measured": peak, "frac_of_seq_read": (nbytes / dt / 1e9 / peak) if peak else None,
+                  "seq_read_GBs_range": [min(all_rates), max(all_rates)] if all_rates else None,
+                  "seq_read_same_request_GBs": same,
+                  "frac_of_same_request_seq_read": (nbytes / dt / 1e9 / max(same)) if same else None,
+                  "seq_read_before": seq_before, "seq_read_after": seq_after,
                   "sampled_step_bit_exact": ok, "files_written_s": write_s}), flush=True)
 L.close()

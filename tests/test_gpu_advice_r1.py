@@ -146,3 +146,31 @@ def test_oversized_record_fails_at_create(pp):
         torch.cuda.synchronize()
         want = oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, 1, F, L.get_order()[:2]))
         assert np.array_equal(_bits16(buf[: 2 * F].view(2, 1, F)), want)
+
+
+def test_pdl_chain_guard_on_reused_slots(pp):
+    # consumer stream == loader stream: consecutive gathers are chained by programmatic dependent
+    # launch, except a launch that rewrites a slot the chain still writes
+    N, H, F, B = 50_000, 4, 32, 1024
+    with pp.Loader(num_nodes=N, num_hops=H, feat_dim=F, dtype=pp.PP_F32, batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.fill_synthetic(1)
+        st = torch.cuda.Stream()
+        L.set_stream(st)
+        bufs = [torch.empty((B, H, F), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+        ring = torch.empty((6, B, H, F), dtype=torch.bfloat16, device="cuda")
+        order = oracle.epoch_order(3, N, 1)
+        with torch.cuda.stream(st):
+            L.epoch_permute(3, 1, st)
+            q0 = L.query()["pdl_launches"]
+            for t in range(6):  # two buffers alternated: calls 2 and 4 reuse buffer 0 -> serialised
+                L.next_batch(bufs[t % 2], None, None, st)
+            q1 = L.query()["pdl_launches"]
+            for t in range(6):  # six distinct slots: every launch after the first is chained
+                L.next_batch(ring[t], None, None, st)
+            q2 = L.query()["pdl_launches"]
+        st.synchronize()
+        assert q1 - q0 == 3 and q2 - q1 == 5, (q1 - q0, q2 - q1)
+        for t in range(6):  # ring slot t holds batch 6 + t
+            want = oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, H, F, order[(6 + t) * B:(7 + t) * B]))
+            assert np.array_equal(_bits16(ring[t]), want), t
+        assert np.array_equal(_bits16(bufs[1]), oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, H, F, order[5 * B:6 * B])))
