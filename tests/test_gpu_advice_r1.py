@@ -165,12 +165,13 @@ def test_pdl_chain_guard_on_reused_slots(pp):
             for t in range(6):  # two buffers alternated: calls 2 and 4 reuse buffer 0 -> serialised
                 L.next_batch(bufs[t % 2], None, None, st)
             q1 = L.query()["pdl_launches"]
+            L.epoch_permute(3, 1, st)  # the epoch again: its first gather is serialised
             for t in range(6):  # six distinct slots: every launch after the first is chained
                 L.next_batch(ring[t], None, None, st)
             q2 = L.query()["pdl_launches"]
         st.synchronize()
         assert q1 - q0 == 3 and q2 - q1 == 5, (q1 - q0, q2 - q1)
-        for t in range(6):  # ring slot t holds batch 6 + t
-            want = oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, H, F, order[(6 + t) * B:(7 + t) * B]))
+        for t in range(6):  # ring slot t holds batch t
+            want = oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, H, F, order[t * B:(t + 1) * B]))
             assert np.array_equal(_bits16(ring[t]), want), t
         assert np.array_equal(_bits16(bufs[1]), oracle.cast_bf16(oracle.gen_rows(1, oracle.F32, H, F, order[5 * B:6 * B])))
