@@ -1,8 +1,10 @@
 // Device-side counter-based Philox4x32-10 (Salmon et al., SC'11), the RNG the
 // north star fixes for the epoch permutation ("a counter-based Philox stream
 // specified once and implemented separately in both oracle and GPU code").
-// Written independently of oracle/pp_oracle.c; the two are compared by the
-// GPU parity tests and this one against curand_Philox4x32_10 on device.
+// Written independently of oracle/pp_oracle.c.  The oracle's Philox, unit-key
+// layout and generator words are pinned against cuRAND's curand_Philox4x32_10 on
+// device (tests/test_gpu_curand_pins.py); this implementation is compared with the
+// oracle through every permutation and synthetic-fill parity test.
 #pragma once
 #include <cstdint>
 
