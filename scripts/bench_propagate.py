@@ -67,7 +67,7 @@ print(json.dumps({"config": "products-sized ER graph", "n": n, "nnz": nnz, "F": 
                   "ms_per_hop": ms / K, "compulsory_bytes_per_hop": compulsory,
                   "compulsory_GBs": compulsory * K / ms / 1e6, "gather_bytes_per_hop": gather_bytes,
                   "gather_GBs": gather_bytes * K / ms / 1e6,
-                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (sliced above 64 MB per hop)")}))
+                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (row kernels; PPLOAD_SPMM=sliced opt-in)")}))
 
 # Same graph, propagated INTO a loader store (pp_propagate_store: node-major [n, K+1, F] fp32
 # records, hop slot k from slot k-1, weights from the degree array on the fly).
@@ -93,7 +93,7 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
 per_hop = nnz * (F * 4 + 8 + 4) + n * (F * 4 + 16)
 print(json.dumps({"config": "products-sized ER graph, into the loader store",
-                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (sliced above 64 MB per hop)"), "n": n,
+                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (row kernels; PPLOAD_SPMM=sliced opt-in)"), "n": n,
                   "nnz": nnz, "F": F, "K": K, "ms": ms, "algorithmic_GBs": K * per_hop / ms / 1e6,
                   "compulsory_GBs": compulsory * K / ms / 1e6, "gather_GBs": gather_bytes * K / ms / 1e6,
                   "frac_hbm": K * per_hop / ms / 1e6 / peak, "ms_per_hop": ms / K}))

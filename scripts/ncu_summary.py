@@ -22,7 +22,10 @@ METRICS = [
     "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
     "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
     "pcie__read_bytes.sum", "pcie__write_bytes.sum", "lts__t_sectors_aperture_sysmem_op_read.sum",
+    "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_requests_srcunit_ltcfabric.sum",
 ]
+SUBSTR = ["pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -62,6 +65,9 @@ def full(src, dst, key=None):
             if m in hdr:
                 i = hdr.index(m)
                 lines.append(f"  {m:62s} {r[i]:>16s} {units[i]}")
+        for i, h in enumerate(hdr):
+            if any(x in h for x in SUBSTR):
+                lines.append(f"  {h.split('.', 2)[-1] if h.count('.') > 3 else h:62s} {r[i]:>16s} {units[i]}")
         try:
             ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             traffic.append(float(r[ir]) * SCALE[units[ir]] + float(r[iw]) * SCALE[units[iw]])
