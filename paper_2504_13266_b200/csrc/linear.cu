@@ -31,6 +31,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -662,7 +664,7 @@ __device__ __forceinline__ uint32_t f16x2(uint32_t lo, uint32_t hi) {
 
 __global__ void __launch_bounds__(kLinThreads, 1)
     k_gather_linear_kc(const LinearArgs a, const __grid_constant__ CUtensorMap zmap,
-                       const __grid_constant__ CUtensorMap wmap) {
+                       const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap) {
   extern __shared__ uint8_t smem_raw[];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kKcAStages; ++s) {
-      bar_init(&a_full[s], kProducerThreads);
+      bar_init(&a_full[s], a.tma_a ? 1 : kProducerThreads);  // TMA gathers: one arrive + the bytes
       bar_init(&a_empty[s], 1);
     }
     for (int s = 0; s < kKcWStages; ++s) {
@@ -735,7 +737,52 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     return total;
   };
 
-  if (warp < kProducerWarps) {
+  if (a.tma_a && warp == 0) {
+    // ---------------- 16-bit records, F % 64 == 0, every row in HBM: the A chunks are the records'
+    // bytes as they are, so TMA fetches them straight into the SW128 A tile: per chunk, 32
+    // cp.async.bulk.tensor tile::gather4 (4 rows x 128 B each) on a 2-D map of the store
+    // [rows][record elements] -- no register staging, all of a chunk's 16 KB in flight at once.
+    // The warp resolves the tile's 128 row indices (order -> node set), lane 0 issues.
+    __shared__ int32_t s_rows[kTileM];
+    const uint64_t amap_addr = reinterpret_cast<uint64_t>(&amap);
+    int64_t u = 0;
+    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+      int64_t step, pos;
+      int r0;
+      const int rows = tile_rows(t, step, r0, pos);
+      __syncwarp();
+      for (int j = lane; j < kTileM; j += 32) {
+        int64_t v = 0;  // rows past the batch gather record 0; the epilogue never stores them
+        if (j < rows) {
+          v = a.order[pos + r0 + j];
+          if (a.node_set != nullptr) v = a.node_set[v];
+        }
+        s_rows[j] = static_cast<int32_t>(v);
+      }
+      __syncwarp();
+      for (int ch = 0; ch < nch; ++ch, ++u) {
+        if (lane == 0) {
+          const int s = static_cast<int>(u % kKcAStages);
+          bar_wait(&a_empty[s], (static_cast<uint32_t>(u / kKcAStages) & 1u) ^ 1u);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&a_full[s])),
+                       "r"(kKcABytes)
+                       : "memory");
+          const int col = k * F + ch * kKcChunk;
+          uint8_t* dst = a_s + s * kKcABytes;
+          for (int g = 0; g < kTileM / 4; ++g)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 512)),
+                "l"(amap_addr), "r"(col), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
+                "r"(s_rows[4 * g + 3]), "r"(smem_addr(&a_full[s]))
+                : "memory");
+        }
+      }
+    }
+    __syncwarp();
+  } else if (a.tma_a && warp < kProducerWarps) {
+    // (idle in the TMA-gather mode)
+  } else if (warp < kProducerWarps) {
     // ---------------- producers: warp w owns rows 16w..16w+15 of every tile.  Lanes 0-15 resolve
     // the 16 row pointers once per tile; per chunk, fp32 records: half-warp per row (lane c loads
     // elements 4c..4c+3 of the chunk, 16 B), 8 iterations; 16-bit records: quarter-warp per row
@@ -1019,6 +1066,20 @@ bool encode_w_map_kc(const LinearArgs& a, CUtensorMap* m) {
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
+// The store as a 2-D map {record element, row} of 16-bit elements (row pitch = the record stride),
+// box 64 elements x 1 row, 128-byte swizzle: each tile::gather4 lands 4 rows x 128 B as rows of
+// the SW128 K-major A chunk.
+bool encode_a_map_kc(const LinearArgs& a, CUtensorMap* m) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (encode == nullptr) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.rec_stride / 2), static_cast<cuuint64_t>(a.shards[0].n_hbm)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.rec_stride)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKcChunk), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace
 
 cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream_t st) {
@@ -1036,6 +1097,15 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   a.z_tma = encode_z_map(a, &zmap) ? 1 : 0;
   alignas(64) CUtensorMap wmap{};
   if (!encode_w_map_kc(a, &wmap)) return cudaErrorNotSupported;
+  // A chunks by TMA gather4: 16-bit records (copied as they are), whole 64-element chunks inside
+  // each hop (F % 64 == 0), one HBM-resident unsharded store
+  alignas(64) CUtensorMap amap{};
+  const char* ta = getenv("PPLOAD_LINEAR_TMA_A");
+  a.tma_a = 0;
+  if (!(ta && !strcmp(ta, "0")) && a.in_dtype != 0 && a.F % kKcChunk == 0 && a.world == 1 &&
+      a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
+      a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
+    a.tma_a = encode_a_map_kc(a, &amap) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
   cfg.blockDim = dim3(kLinThreads);
@@ -1046,7 +1116,7 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   lattr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gather_linear_kc, a, zmap, wmap);
+  return cudaLaunchKernelEx(&cfg, k_gather_linear_kc, a, zmap, wmap, amap);
 }
 
 }  // namespace ppl

@@ -157,3 +157,20 @@ def test_kc_local_epoch(pp):
     finally:
         for L_ in Ls:
             L_.close()
+
+
+@pytest.mark.parametrize("tma_a", ["1", "0"])
+@pytest.mark.parametrize("dt,F,chunk", [(oracle.F16, 768, 1), (oracle.BF16, 128, 7), (oracle.F16, 192, 64)])
+def test_kc_tma_gather4_sixteen_bit(pp, monkeypatch, tma_a, dt, F, chunk):
+    # 16-bit records with F % 64 == 0 in HBM: the A chunks come straight from the store by TMA
+    # tile::gather4 (PPLOAD_LINEAR_TMA_A=1, default) or through the register-staged producers (0);
+    # node set + ragged last step included
+    monkeypatch.setenv("PPLOAD_LINEAR_TMA_A", tma_a)
+    H, N, B, D = 3, 2500, 384, 256
+    X, hs, rs = hop_tensor(78 + F, H, N, F, dtype=np.uint16)
+    S = make_node_set(79, N, 2101)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=dt,
+                   node_set=S, batch_size=B, out_dtype=dt) as L:
+        L.epoch_permute(10, chunk)
+        order = oracle.epoch_order(10, S.shape[0], chunk, node_set=S)
+        run_and_check(pp, L, X, dt, hs, rs, H, F, D, order, B, dt, "f32", k=3)
