@@ -1100,9 +1100,12 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   // A chunks by TMA gather4: 16-bit records (copied as they are), whole 64-element chunks inside
   // each hop (F % 64 == 0), one HBM-resident unsharded store
   alignas(64) CUtensorMap amap{};
+  // Opt-in (PPLOAD_LINEAR_TMA_A=1): measured slower than the register-staged producers at the
+  // MAG240M row shape (21.4 vs 18.5 ms per 4 M-row epoch, profiles/r2/fused_linear_kc_tma_gather4.jsonl):
+  // the kernel is bound by the W_k chunks streamed from L2 (786 KB per 128-row tile), not by A
   const char* ta = getenv("PPLOAD_LINEAR_TMA_A");
   a.tma_a = 0;
-  if (!(ta && !strcmp(ta, "0")) && a.in_dtype != 0 && a.F % kKcChunk == 0 && a.world == 1 &&
+  if (ta && !strcmp(ta, "1") && a.in_dtype != 0 && a.F % kKcChunk == 0 && a.world == 1 &&
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
     a.tma_a = encode_a_map_kc(a, &amap) ? 1 : 0;

@@ -163,7 +163,7 @@ def test_kc_local_epoch(pp):
 @pytest.mark.parametrize("dt,F,chunk", [(oracle.F16, 768, 1), (oracle.BF16, 128, 7), (oracle.F16, 192, 64)])
 def test_kc_tma_gather4_sixteen_bit(pp, monkeypatch, tma_a, dt, F, chunk):
     # 16-bit records with F % 64 == 0 in HBM: the A chunks come straight from the store by TMA
-    # tile::gather4 (PPLOAD_LINEAR_TMA_A=1, default) or through the register-staged producers (0);
+    # tile::gather4 (PPLOAD_LINEAR_TMA_A=1, opt-in) or through the register-staged producers (0, default);
     # node set + ragged last step included
     monkeypatch.setenv("PPLOAD_LINEAR_TMA_A", tma_a)
     H, N, B, D = 3, 2500, 384, 256
