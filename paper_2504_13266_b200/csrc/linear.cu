@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -737,12 +738,14 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     return total;
   };
 
-  if (a.tma_a && warp == 0) {
+  const int gw = a.tma_a >= 2 ? 8 : 4;  // warps issuing gather4 (tma_a = 2: all eight producer warps)
+  if (a.tma_a && warp < gw) {
     // ---------------- 16-bit records, F % 64 == 0, every row in HBM: the A chunks are the records'
     // bytes as they are, so TMA fetches them straight into the SW128 A tile: per chunk, 32
     // cp.async.bulk.tensor tile::gather4 (4 rows x 128 B each) on a 2-D map of the store
     // [rows][record elements] -- no register staging, all of a chunk's 16 KB in flight at once.
-    // The warp resolves the tile's 128 row indices (order -> node set), lane 0 issues.
+    // Warp w (0..3) resolves rows 32w..32w+31 of the tile (order -> node set) and its lane 0 issues
+    // their 8 gather4s; warp 0 also posts the stage's expected bytes.
     __shared__ int32_t s_rows[kTileM];
     const uint64_t amap_addr = reinterpret_cast<uint64_t>(&amap);
     int64_t u = 0;
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       int r0;
       const int rows = tile_rows(t, step, r0, pos);
       __syncwarp();
-      for (int j = lane; j < kTileM; j += 32) {
+      for (int j = warp * (kTileM / gw) + lane; j < (warp + 1) * (kTileM / gw); j += 32) {
         int64_t v = 0;  // rows past the batch gather record 0; the epilogue never stores them
         if (j < rows) {
           v = a.order[pos + r0 + j];
@@ -764,12 +767,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         if (lane == 0) {
           const int s = static_cast<int>(u % kKcAStages);
           bar_wait(&a_empty[s], (static_cast<uint32_t>(u / kKcAStages) & 1u) ^ 1u);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&a_full[s])),
-                       "r"(kKcABytes)
-                       : "memory");
+          if (warp == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&a_full[s])),
+                         "r"(kKcABytes)
+                         : "memory");
           const int col = k * F + ch * kKcChunk;
           uint8_t* dst = a_s + s * kKcABytes;
-          for (int g = 0; g < kTileM / 4; ++g)
+          for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 512)),
@@ -780,7 +784,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
     }
     __syncwarp();
-  } else if (a.tma_a && warp < kProducerWarps) {
+  } else if (a.tma_a && warp < kProducerWarps) {  // warps 4-7
     // (idle in the TMA-gather mode)
   } else if (warp < kProducerWarps) {
     // ---------------- producers: warp w owns rows 16w..16w+15 of every tile.  Lanes 0-15 resolve
@@ -870,32 +874,57 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                      : "memory");
       }
     };
-    uint4 xa[8], xb[8];
+    // Register ring of R chunks: the loads of unit u + R - 1 are issued before unit u is converted
+    // and stored, across tile boundaries.  R = 2 for fp32 records (8 x 16 B per lane and chunk),
+    // R = 4 for 16-bit records (4 x 16 B): 64 registers of loads in flight either way.
     int64_t u = 0;  // unit counter: (tile, chunk) pairs in order
-    int64_t t = next_tile(q);
-    const uint8_t* src = t < total ? resolve(fetch_index(t)) : nullptr;
-    int64_t t_next = t < total ? next_tile(t + Q) : total;
-    const uint8_t* src_next = t_next < total ? resolve(fetch_index(t_next)) : nullptr;
-    for (int d = 0; d < pf; ++d) prefetch_chunk(d < nch ? src : src_next, d < nch ? d : d - nch);
-    while (t < total) {
-      load_chunk(src, 0, xa);
-      for (int ch = 0; ch < nch; ++ch) {
-        const int p = ch + pf;  // the unit pf ahead: this tile or the next one
-        if (pf > 0) prefetch_chunk(p < nch ? src : src_next, p < nch ? p : p - nch);
-        // issue chunk ch + 1 before storing chunk ch (the two register buffers alternate)
-        if (ch % 2 == 0) {
-          if (ch + 1 < nch) load_chunk(src, ch + 1, xb);
-          store_chunk(u++, xa);
-        } else {
-          if (ch + 1 < nch) load_chunk(src, ch + 1, xa);
-          store_chunk(u++, xb);
+    int64_t lt = next_tile(q);  // the load cursor: tile, chunk, this lane's row pointer
+    int lch = 0;
+    const uint8_t* lsrc = lt < total ? resolve(fetch_index(lt)) : nullptr;
+    int64_t pt = lt < total ? next_tile(lt + Q) : total;  // the L2-prefetch cursor, pf units ahead
+    int pch = 0;
+    const uint8_t* psrc = pt < total ? resolve(fetch_index(pt)) : nullptr;
+    auto load_next = [&](uint4 (&buf)[8]) -> bool {
+      if (lt >= total) return false;
+      load_chunk(lsrc, lch, buf);
+      if (++lch == nch) {
+        lch = 0;
+        lt = next_tile(lt + Q);
+        lsrc = lt < total ? resolve(fetch_index(lt)) : nullptr;
+      }
+      return true;
+    };
+    auto run = [&](auto ring) {
+      constexpr int R = decltype(ring)::value;
+      uint4 x[R][8];
+      bool have[R];
+#pragma unroll
+      for (int j = 0; j < R - 1; ++j) have[j] = load_next(x[j]);
+      have[R - 1] = false;
+      for (;;) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int jn = (j + R - 1) % R;
+          have[jn] = load_next(x[jn]);
+          if (pf > 0 && pt < total) {  // bulk L2 prefetch of the chunk pf units ahead of the loads
+            prefetch_chunk(psrc, pch);
+            if (++pch == nch) {
+              pch = 0;
+              pt = next_tile(pt + Q);
+              psrc = pt < total ? resolve(fetch_index(pt)) : nullptr;
+            }
+          }
+          if (!have[j]) return;
+          store_chunk(u++, x[j]);
         }
       }
-      t = t_next;
-      src = src_next;
-      t_next = t < total ? next_tile(t + Q) : total;
-      src_next = t_next < total ? resolve(fetch_index(t_next)) : nullptr;
-    }
+    };
+    if (f32)
+      run(std::integral_constant<int, 2>{});
+    else
+      run(std::integral_constant<int, 4>{});
   } else if (warp == kKcLoaderWarp) {
     // ---------------- W loader: the same (tile, chunk) sequence; chunk ch of W_k into stage u % 2
     if (lane == 0) {
@@ -932,24 +961,33 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
         for (int ch = 0; ch < nch; ++ch, ++u) {
           const int sa = static_cast<int>(u % kKcAStages), sw = static_cast<int>(u % kKcWStages);
-          if (ch == 0)
-            for (int h = 0; h < nh; ++h) bar_wait(&t_empty[h], (i & 1) ^ 1);
           bar_wait(&a_full[sa], static_cast<uint32_t>(u / kKcAStages) & 1u);
           bar_wait(&w_full[sw], static_cast<uint32_t>(u / kKcWStages) & 1u);
           tc_fence_after();
           const uint8_t* at = a_s + sa * kKcABytes;
           const uint8_t* wt = w_s + sw * w_stage_bytes;
-          for (int h = 0; h < ((a.debug & 64) ? 0 : nh); ++h) {
+          if (ch == 0 && (a.debug & 512)) {  // experiment: both accumulators drained before the tile starts
+            for (int h = 0; h < nh; ++h) bar_wait(&t_empty[h], (i & 1) ^ 1);
+            tc_fence_after();
+          }
+          for (int h = 0; h < nh; ++h) {
+            if (ch == 0 && !(a.debug & 512)) {  // accumulator h of the previous tile drained (the epilogue
+              bar_wait(&t_empty[h], (i & 1) ^ 1);  // drains h = 0 first, so h = 0 MMAs overlap the h = 1 drain)
+              tc_fence_after();
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < ((a.debug & 64) ? 0 : 4); ++j) {
               const uint64_t ad = sw128_desc(at) + 2 * j;                             // +32 B per 16 K
               const uint64_t bd = kc_w_desc(wt + h * (kUmmaN / 64) * kKcWBox + j * 2048);  // 16 K rows per step
               umma_i(tmem + h * kUmmaN, ad, bd, idesc, (ch > 0 || j > 0) ? 1u : 0u);
             }
+            // last chunk: accumulator h is complete once these MMAs are -- the epilogue can start
+            // draining it while the other accumulator's last MMAs run
+            if (ch == nch - 1 && !(a.debug & 1024)) umma_commit(&t_full[h]);
           }
           umma_commit(&a_empty[sa]);
           umma_commit(&w_empty[sw]);
-          if (ch == nch - 1)
+          if (ch == nch - 1 && (a.debug & 1024))  // experiment: both accumulators committed after the unit
             for (int h = 0; h < nh; ++h) umma_commit(&t_full[h]);
         }
       }
@@ -1100,15 +1138,16 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   // A chunks by TMA gather4: 16-bit records (copied as they are), whole 64-element chunks inside
   // each hop (F % 64 == 0), one HBM-resident unsharded store
   alignas(64) CUtensorMap amap{};
-  // Opt-in (PPLOAD_LINEAR_TMA_A=1): measured slower than the register-staged producers at the
-  // MAG240M row shape (21.4 vs 18.5 ms per 4 M-row epoch, profiles/r2/fused_linear_kc_tma_gather4.jsonl):
-  // the kernel is bound by the W_k chunks streamed from L2 (786 KB per 128-row tile), not by A
+  // Default for eligible stores; PPLOAD_LINEAR_TMA_A=0 forces the register-staged producers,
+  // =2 spreads the gather4 issue over all eight producer warps (r2: one issuing lane 21.4 ms, four
+  // warps 12.6 ms, register producers 14.8 ms per MAG240M-row epoch)
   const char* ta = getenv("PPLOAD_LINEAR_TMA_A");
+  const int want_tma = ta ? atoi(ta) : 1;
   a.tma_a = 0;
-  if (ta && !strcmp(ta, "1") && a.in_dtype != 0 && a.F % kKcChunk == 0 && a.world == 1 &&
+  if (want_tma > 0 && a.in_dtype != 0 && a.F % kKcChunk == 0 && a.world == 1 &&
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
-    a.tma_a = encode_a_map_kc(a, &amap) ? 1 : 0;
+    a.tma_a = encode_a_map_kc(a, &amap) ? want_tma : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
   cfg.blockDim = dim3(kLinThreads);

@@ -1468,7 +1468,7 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   a.world = L->W;
   for (int i = 0; i < kMaxWorld; ++i) a.shards[i] = ShardView{L->shards[i].hbm, L->shards[i].spill, L->shards[i].n_hbm};
   if (const char* e = getenv("PPLOAD_DEBUG_LINEAR")) a.debug = atoi(e);
-  a.l2_prefetch = resident ? 1 : 4;  // resident kernel: next tile's rows; K-chunked: chunks ahead
+  a.l2_prefetch = resident ? 1 : 0;  // resident kernel: next tile's rows; K-chunked: off (r2 sweep: no gain)
   if (const char* e = getenv("PPLOAD_LINEAR_PREFETCH")) a.l2_prefetch = atoi(e);
   static uint64_t* dbg_ts = nullptr;  // experiment probe: timestamps of CTA 0 (PPLOAD_DEBUG_TS=1)
   const bool want_ts = resident && getenv("PPLOAD_DEBUG_TS") != nullptr;
