@@ -37,6 +37,8 @@
  *   - One handle is used by one host thread at a time.
  *   - "stream" arguments are cudaStream_t values passed as void*; NULL is the
  *     legacy default stream.
+ *   - Tracing: every call opens an NVTX range named after it (nsys / ncu
+ *     timelines; no cost beyond a few ns without a tool attached).
  */
 #ifndef PP_LOADER_H
 #define PP_LOADER_H

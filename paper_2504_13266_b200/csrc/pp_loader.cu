@@ -23,6 +23,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/pp_loader.h"
 #include "internal.h"
 
@@ -44,6 +46,15 @@ pp_status fail(pp_status st, const char* fmt, ...) {
 
 int elem_bytes(pp_dtype d) { return d == PP_F32 ? 4 : 2; }
 bool valid_dtype(int d) { return d == PP_F32 || d == PP_BF16 || d == PP_F16; }
+
+// NVTX range around each public call (nsys / ncu timelines show the loader's host-side phases; the
+// header-only NVTX API costs a few ns when no tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DevGuard {
   int prev = -1;
@@ -460,6 +471,7 @@ const char* pp_last_error(void) { return g_last_error.c_str(); }
 
 pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64_t* col_idx, const float* X,
                        int32_t K, float* hops, void* stream) {
+  NvtxRange nvtx_range("pp_propagate");
   if (n < 1 || F < 1 || F > 256 || K < 0) return fail(PP_ERR_INVALID, "need n >= 1, 1 <= F <= 256, K >= 0");
   if (!row_ptr || !col_idx || !X || !hops) return fail(PP_ERR_INVALID, "NULL pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -536,6 +548,7 @@ int64_t pp_footprint_bytes(int64_t num_nodes, int32_t feat_dim, int32_t elem_byt
 }
 
 pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
+  NvtxRange nvtx_range("pp_loader_create");
   if (!out) return fail(PP_ERR_INVALID, "out is NULL");
   *out = nullptr;
   pp_status st = validate(desc);
@@ -743,6 +756,7 @@ pp_status pp_loader_destroy(pp_loader* L) {
 
 pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, const int64_t* col_idx,
                              const int32_t* deg, void* stream) {
+  NvtxRange nvtx_range("pp_propagate_store");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!row_ptr || !col_idx || !deg) return fail(PP_ERR_INVALID, "NULL CSR / degree pointer");
@@ -874,6 +888,7 @@ static pp_status enqueue_order(pp_loader* L, uint64_t seed, int64_t chunk, uint3
 // from local HBM and no exchange is needed at any W.  Local position lr maps
 // to global node lr * W + rank.  Not collective; ranks may use different seeds.
 pp_status pp_epoch_permute_local(pp_loader* L, uint64_t seed, int64_t chunk, void* stream) {
+  NvtxRange nvtx_range("pp_epoch_permute_local");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (L->d_node_set) return fail(PP_ERR_INVALID, "local shuffling is defined without a node set");
@@ -995,6 +1010,7 @@ static pp_status build_a2a_counts(pp_loader* L) {
 }
 
 pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* stream) {
+  NvtxRange nvtx_range("pp_epoch_permute");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
@@ -1064,6 +1080,7 @@ pp_status pp_epoch_permute(pp_loader* L, uint64_t seed, int64_t chunk, void* str
 }
 
 pp_status pp_epoch_prefetch(pp_loader* L, uint64_t seed, int64_t chunk) {
+  NvtxRange nvtx_range("pp_epoch_prefetch");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (chunk < 1 || chunk > L->N) return fail(PP_ERR_INVALID, "chunk must be in [1, N=%lld]", (long long)L->N);
@@ -1334,6 +1351,7 @@ static pp_status enqueue_a2a_steps(pp_loader* L, int64_t nsteps, const StepOut& 
 
 static pp_status next_steps(pp_loader* L, int32_t n, void* out, int64_t out_stride, int32_t* out_labels,
                             int64_t* out_nodes, int32_t* rows, int32_t* n_done, const Handoff& ho) {
+  NvtxRange nvtx_range("pp_next_batches");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1) return fail(PP_ERR_INVALID, "rows is NULL or n < 1");
@@ -1410,6 +1428,7 @@ pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_str
 
 pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t D, void* Z, pp_dtype z_dtype,
                                  int64_t z_stride_bytes, int32_t* rows, int32_t* n_done, void* consumer_stream) {
+  NvtxRange nvtx_range("pp_next_batches_linear");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (!rows || n < 1 || !W || !Z) return fail(PP_ERR_INVALID, "NULL argument or n < 1");
@@ -1559,6 +1578,7 @@ pp_status pp_loader_query(const pp_loader* L, pp_loader_info* info) {
 }
 
 pp_status pp_fill_synthetic(pp_loader* L, uint64_t data_seed) {
+  NvtxRange nvtx_range("pp_fill_synthetic");
   if (!L) return fail(PP_ERR_INVALID, "loader is NULL");
   if (L->poisoned) return fail(PP_ERR_CUDA, "loader is poisoned by an earlier CUDA error");
   if (L->in_dtype == PP_BF16) return fail(PP_ERR_INVALID, "no synthetic generator for bf16 stores");
@@ -1654,6 +1674,7 @@ static bool nonzero(const uint8_t* p, int n) {
 }
 
 pp_status pp_import_peer_stores(pp_loader* L, const void* handles) {
+  NvtxRange nvtx_range("pp_import_peer_stores");
   if (!L || !handles) return fail(PP_ERR_INVALID, "NULL argument");
   if (L->desc.peers != PP_PEERS_IPC) return fail(PP_ERR_INVALID, "pp_import_peer_stores needs PP_PEERS_IPC");
   if (L->linked) return fail(PP_ERR_STATE, "peers already imported");
