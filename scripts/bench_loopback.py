@@ -4,7 +4,9 @@ round-robin over W loopback shards (PP_PEERS_LOOPBACK: W loader handles in one p
 the global epoch with the sharded gather kernel (owner table, exchange-copy reads of remote
 rows).  No NVLink is involved: this measures the sharded kernel's own efficiency, not the
 link.  Timed: whole epochs of all W ranks (k = 8 steps per launch), CUDA events.  One JSON
-line per W."""
+line per W.  LOOPBACK_EXCHANGE=a2a: the all-to-all path instead (count table at the permute;
+per step the index kernel, the pack by the gather kernel straight into the receive buffer and the
+unpack -- the NCCL transfer itself is what loopback skips)."""
 import json
 import os
 import sys
@@ -20,7 +22,10 @@ import paper_2504_13266_b200 as pp  # noqa: E402
 N, H, F, B, K = 2_449_029, 4, 100, 8192, 8
 PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 st = torch.cuda.Stream()
-for W in (1, 2, 4, 8):
+A2A = os.environ.get("LOOPBACK_EXCHANGE") == "a2a"
+if A2A:
+    os.environ["PPLOAD_EXCHANGE"] = "a2a"
+for W in ((2, 4, 8) if A2A else (1, 2, 4, 8)):
     Ls = []
     for r in range(W):
         kw = dict(world_size=W, rank=r, peers=pp.PP_PEERS_LOOPBACK) if W > 1 else {}
@@ -62,7 +67,10 @@ for W in (1, 2, 4, 8):
     remote = (W - 1) / W
     rd = (1 - remote) * H * F * 4 + remote * H * F * (2 if xcast else 4)
     per_node = rd + H * F * 2 + 4
-    print(json.dumps({"W": W, "exchange_cast": bool(xcast), "gather_ms_per_epoch_all_ranks": ms, "nodes_per_s": N / ms * 1e3,
+    if A2A:  # pack: fp32 record read + cast row written; unpack: cast row read + written; + order
+        per_node = H * F * 4 + 3 * H * F * 2 + 4
+    print(json.dumps({"W": W, "exchange": "a2a (loopback, no transport)" if A2A else "peer reads",
+                      "exchange_cast": bool(xcast), "gather_ms_per_epoch_all_ranks": ms, "nodes_per_s": N / ms * 1e3,
                       "hbm_bytes_per_node": per_node, "achieved_GBs": N * per_node / ms / 1e6,
                       "frac_hbm": N * per_node / ms / 1e6 / PEAK,
                       "note": "gathers of all W ranks, serialised on one GPU; permutations excluded"}),
