@@ -634,15 +634,18 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, bool pdl, cudaStream_t 
 //   and sharded stores work; peer rows are read as store records (not the exchange copy).
 namespace {
 constexpr int kKcChunk = 64;                     // K elements per chunk (one 128-B swizzle row of bf16)
-constexpr int kKcAStages = 4;
-constexpr int kKcWStages = 2;
+// Shared memory at D = 512 (224 KB): 2 W stages of a whole 64-row chunk (128 KB) + 4 slots of 16 KB
+// (A stages; with fp32 records gathered by TMA, 2 A stages + 2 fp32 staging halves) + the epilogue
+// staging (32 KB).  Experiment layout (debug bit 2048): 3 half-chunk W stages (96 KB) + 6 slots.
+constexpr int kKcASlots = 6;   // max 16 KB A / staging slots
+constexpr int kKcWStages = 4;  // max W stages of one 32-row half chunk (D / 64 boxes of 32 x 64)
 constexpr int kKcABytes = kTileM * 128;          // 16 KB: 128 rows x 64 bf16
-constexpr int kKcWBox = kKcChunk * 128;          // 8 KB: 64 K rows x 64 columns
-constexpr int kKcWMaxBytes = (512 / 64) * kKcWBox;  // 64 KB per W stage at D = 512
+constexpr int kKcWBox = (kKcChunk / 2) * 128;    // 4 KB: 32 K rows x 64 columns (one half chunk)
 constexpr int kKcLoaderWarp = 9;
 
-__device__ __forceinline__ uint64_t kc_w_desc(const void* p) {  // MN-major SW128, LBO = 8 KB between boxes
-  return static_cast<uint64_t>((smem_addr(p) >> 4) & 0x3FFFu) | (static_cast<uint64_t>(kKcWBox >> 4) << 16) |
+// MN-major SW128 B descriptor; lbo = bytes between 64-column blocks (the K rows of a stage x 128 B)
+__device__ __forceinline__ uint64_t kc_w_desc(const void* p, uint32_t lbo) {
+  return static_cast<uint64_t>((smem_addr(p) >> 4) & 0x3FFFu) | (static_cast<uint64_t>(lbo >> 4) << 16) |
          (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 __device__ __forceinline__ uint32_t kc_idesc(int out_dtype) {
@@ -670,18 +673,29 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int D = a.D;
-  const int w_stage_bytes = (D / 64) * kKcWBox;
-  uint8_t* w_s = smem;                                    // [kKcWStages][D / 64 boxes][64 K rows][128 B]
-  uint8_t* a_s = w_s + kKcWStages * w_stage_bytes;        // [kKcAStages][128 rows][128 B]
-  uint8_t* z_s = a_s + kKcAStages * kKcABytes;            // epilogue staging
+  // Default: whole-chunk W stages (2 x 64 KB at D = 512) and 4 slots (fp32 gathers: 2 A stages + 2
+  // staging halves).  Experiment bit 2048: 3 half-chunk W stages + 6 slots (measured slower in
+  // interleaved A/B runs: IGB-large rows 26 vs 20 ms, MAG240M rows 24 vs 16 ms, r2x).
+  const bool six = (a.debug & 2048) != 0;
+  const int wsplit = six ? 2 : 1;                         // W stages per chunk
+  const int wrows = kKcChunk / wsplit;                    // K rows per W stage
+  const int w_stage_bytes = (D / 64) * wrows * 128;
+  const int nws = six ? 3 : 2;                            // W stages
+  const int nas = six ? 6 : 4;                            // A / staging slots
+  const int nstg = nas - 2;                               // fp32 staging halves (tma_f32)
+  uint8_t* w_s = smem;                                    // [nws][D / 64 blocks][wrows K rows][128 B]
+  uint8_t* a_s = w_s + nws * w_stage_bytes;               // [nas][128 rows][128 B]
+  uint8_t* z_s = w_s + 4 * ((512 / 64) * kKcWBox) + 4 * kKcABytes;  // epilogue staging (fixed offset)
   uint64_t* bars = reinterpret_cast<uint64_t*>(z_s + kEpiWarps * kEpiBufs * kStageBytes);
-  uint64_t* a_full = bars;                                // [kKcAStages]
-  uint64_t* a_empty = a_full + kKcAStages;                // [kKcAStages]
-  uint64_t* w_full = a_empty + kKcAStages;                // [kKcWStages]
+  uint64_t* a_full = bars;                                // [kKcASlots]
+  uint64_t* a_empty = a_full + kKcASlots;                 // [kKcASlots]
+  uint64_t* w_full = a_empty + kKcASlots;                 // [kKcWStages]
   uint64_t* w_empty = w_full + kKcWStages;                // [kKcWStages]
   uint64_t* t_full = w_empty + kKcWStages;                // [2]
   uint64_t* t_empty = t_full + 2;                         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* stg_full = t_empty + 2;                       // [4] fp32 staging halves (tma_f32)
+  uint64_t* stg_empty = stg_full + 4;                     // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, F = a.F;
@@ -690,13 +704,22 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   const int nh = D / kUmmaN;
   const int nch = (F + kKcChunk - 1) / kKcChunk;
   const int s_in = a.in_dtype == 0 ? 4 : 2;
+  // A stages: 6 (16-bit TMA gathers), 4 (register producers), 2 (fp32 TMA gathers, whose slots 2-5
+  // hold four fp32 staging halves of 128 rows x 32 fp32, SW128)
+  const int na = a.tma_f32 ? 2 : nas;
+  uint8_t* stg = a_s + 2 * kKcABytes;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kKcAStages; ++s) {
-      bar_init(&a_full[s], a.tma_a ? 1 : kProducerThreads);  // TMA gathers: one arrive + the bytes
+    for (int s = 0; s < kKcASlots; ++s) {
+      // arrivals: TMA gathers (16-bit) one arrive + the bytes; fp32 converters 128; register producers 256
+      bar_init(&a_full[s], a.tma_a ? 1 : a.tma_f32 ? 128 : kProducerThreads);
       bar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < kKcWStages; ++s) {
+    for (int s = 0; s < 4; ++s) {
+      bar_init(&stg_full[s], 1);
+      bar_init(&stg_empty[s], 128);
+    }
+    for (int s = 0; s < kKcWStages; ++s) {  // (only the first nws are used)
       bar_init(&w_full[s], 1);
       bar_init(&w_empty[s], 1);
     }
@@ -739,7 +762,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   };
 
   const int gw = a.tma_a >= 2 ? 8 : 4;  // warps issuing gather4 (tma_a = 2: all eight producer warps)
-  if (a.tma_a && warp < gw) {
+  if ((a.tma_a || a.tma_f32) && warp < gw) {
     // ---------------- 16-bit records, F % 64 == 0, every row in HBM: the A chunks are the records'
     // bytes as they are, so TMA fetches them straight into the SW128 A tile: per chunk, 32
     // cp.async.bulk.tensor tile::gather4 (4 rows x 128 B each) on a 2-D map of the store
@@ -764,9 +787,32 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       __syncwarp();
       for (int ch = 0; ch < nch; ++ch, ++u) {
+        if (a.tma_f32) {  // fp32 records: two 32-element halves into the staging slots, converted by warps 4-7
+          if (lane == 0) {
+            for (int hh = 0; hh < 2; ++hh) {
+              const int64_t v = 2 * u + hh;  // staging half v in slot v % nstg
+              const int sl = static_cast<int>(v % nstg);
+              bar_wait(&stg_empty[sl], (static_cast<uint32_t>(v / nstg) & 1u) ^ 1u);
+              if (warp == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[sl])),
+                             "r"(kKcABytes)
+                             : "memory");
+              const int col = k * F + ch * kKcChunk + hh * 32;
+              uint8_t* dst = stg + sl * kKcABytes;
+              for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 512)),
+                    "l"(amap_addr), "r"(col), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
+                    "r"(s_rows[4 * g + 3]), "r"(smem_addr(&stg_full[sl]))
+                    : "memory");
+            }
+          }
+          continue;
+        }
         if (lane == 0) {
-          const int s = static_cast<int>(u % kKcAStages);
-          bar_wait(&a_empty[s], (static_cast<uint32_t>(u / kKcAStages) & 1u) ^ 1u);
+          const int s = static_cast<int>(u % na);
+          bar_wait(&a_empty[s], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
           if (warp == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&a_full[s])),
                          "r"(kKcABytes)
@@ -784,6 +830,40 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
     }
     __syncwarp();
+  } else if (a.tma_f32 && warp < kProducerWarps) {
+    // ---------------- fp32 records gathered by TMA: warps 4-7 convert the staged halves (SW128 fp32,
+    // 32 per row) into the SW128 bf16 / f16 A chunk: thread (row r, 16-B A chunk j of the half) reads
+    // staged chunks 2j, 2j+1 (8 fp32), converts with cvt.rn, writes one 16-byte A chunk.
+    const int tid = threadIdx.x - 128;
+    int64_t u = 0;
+    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+      for (int ch = 0; ch < nch; ++ch, ++u) {
+        const int sa = static_cast<int>(u % na);
+        bar_wait(&a_empty[sa], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
+        uint8_t* at = a_s + sa * kKcABytes;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int64_t v = 2 * u + hh;
+          const int sl = static_cast<int>(v % nstg);
+          bar_wait(&stg_full[sl], static_cast<uint32_t>(v / nstg) & 1u);
+          const uint8_t* sh = stg + sl * kKcABytes;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int item = tid + 128 * it;
+            const int r = item >> 2, j = item & 3;
+            const uint4 x0 = *reinterpret_cast<const uint4*>(sh + r * 128 + (((2 * j) ^ (r & 7)) << 4));
+            const uint4 x1 = *reinterpret_cast<const uint4*>(sh + r * 128 + (((2 * j + 1) ^ (r & 7)) << 4));
+            const uint4 y = a.out_dtype == 2
+                                ? make_uint4(f16x2(x0.x, x0.y), f16x2(x0.z, x0.w), f16x2(x1.x, x1.y), f16x2(x1.z, x1.w))
+                                : make_uint4(bf16x2(x0.x, x0.y), bf16x2(x0.z, x0.w), bf16x2(x1.x, x1.y),
+                                             bf16x2(x1.z, x1.w));
+            *reinterpret_cast<uint4*>(at + sw128(r, hh * 4 + j)) = y;
+          }
+          bar_arrive(&stg_empty[sl]);
+        }
+        fence_async_smem();
+        bar_arrive(&a_full[sa]);
+      }
+    }
   } else if (a.tma_a && warp < kProducerWarps) {  // warps 4-7
     // (idle in the TMA-gather mode)
   } else if (warp < kProducerWarps) {
@@ -839,8 +919,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
     };
     auto store_chunk = [&](int64_t u, const uint4 (&x)[8]) {
-      const int s = static_cast<int>(u % kKcAStages);
-      bar_wait(&a_empty[s], (static_cast<uint32_t>(u / kKcAStages) & 1u) ^ 1u);
+      const int s = static_cast<int>(u % na);
+      bar_wait(&a_empty[s], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
       uint8_t* at = a_s + s * kKcABytes;
       if (f32) {
 #pragma unroll
@@ -930,24 +1010,28 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     if (lane == 0) {
       const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
       const uint32_t nbox = static_cast<uint32_t>(D / 64);
-      int64_t u = 0;
+      int64_t wv = 0;  // W stage-fill counter: (tile, chunk, part) in order
       for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
-        for (int ch = 0; ch < nch; ++ch, ++u) {
-          const int s = static_cast<int>(u % kKcWStages);
-          bar_wait(&w_empty[s], (static_cast<uint32_t>(u / kKcWStages) & 1u) ^ 1u);
-          if (a.debug & 16) {  // experiment: no W traffic (the MMAs read stale shared memory)
-            bar_arrive(&w_full[s]);
-            continue;
+        for (int ch = 0; ch < nch; ++ch) {
+          for (int wh = 0; wh < wsplit; ++wh, ++wv) {
+            const int s = static_cast<int>(wv % nws);
+            bar_wait(&w_empty[s], (static_cast<uint32_t>(wv / nws) & 1u) ^ 1u);
+            if (a.debug & 16) {  // experiment: no W traffic (the MMAs read stale shared memory)
+              bar_arrive(&w_full[s]);
+              continue;
+            }
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&w_full[s])),
+                         "r"(w_stage_bytes)
+                         : "memory");
+            for (uint32_t b = 0; b < nbox; ++b)
+              for (int sub = 0; sub < wrows / 32; ++sub)  // 32-row boxes stacked inside the 64-column block
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                    "%4}], [%5];" ::"r"(smem_addr(w_s + s * w_stage_bytes + b * wrows * 128 + sub * kKcWBox)),
+                    "l"(wmap_addr), "r"(static_cast<int>(b * 64)), "r"(ch * kKcChunk + wh * wrows + sub * 32), "r"(k),
+                    "r"(smem_addr(&w_full[s]))
+                    : "memory");
           }
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&w_full[s])),
-                       "r"(nbox * kKcWBox)
-                       : "memory");
-          for (uint32_t b = 0; b < nbox; ++b)
-            asm volatile(
-                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-                "[%5];" ::"r"(smem_addr(w_s + s * w_stage_bytes + b * kKcWBox)),
-                "l"(wmap_addr), "r"(static_cast<int>(b * 64)), "r"(ch * kKcChunk), "r"(k), "r"(smem_addr(&w_full[s]))
-                : "memory");
         }
       }
     }
@@ -956,39 +1040,39 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // ---------------- MMA issuer: per unit, 4 K-steps of 16 into each accumulator
     if (lane == 0) {
       const uint32_t idesc = kc_idesc(a.out_dtype);
-      int64_t u = 0;
+      int64_t u = 0, wv = 0;
       int i = 0;
       for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
         for (int ch = 0; ch < nch; ++ch, ++u) {
-          const int sa = static_cast<int>(u % kKcAStages), sw = static_cast<int>(u % kKcWStages);
-          bar_wait(&a_full[sa], static_cast<uint32_t>(u / kKcAStages) & 1u);
-          bar_wait(&w_full[sw], static_cast<uint32_t>(u / kKcWStages) & 1u);
+          const int sa = static_cast<int>(u % na);
+          bar_wait(&a_full[sa], static_cast<uint32_t>(u / na) & 1u);
           tc_fence_after();
           const uint8_t* at = a_s + sa * kKcABytes;
-          const uint8_t* wt = w_s + sw * w_stage_bytes;
-          if (ch == 0 && (a.debug & 512)) {  // experiment: both accumulators drained before the tile starts
-            for (int h = 0; h < nh; ++h) bar_wait(&t_empty[h], (i & 1) ^ 1);
+          // the chunk's W in wsplit stages (whole, or K rows 0-31 and 32-63)
+          for (int wh = 0; wh < wsplit; ++wh, ++wv) {
+            const int sw = static_cast<int>(wv % nws);
+            bar_wait(&w_full[sw], static_cast<uint32_t>(wv / nws) & 1u);
             tc_fence_after();
-          }
-          for (int h = 0; h < nh; ++h) {
-            if (ch == 0 && !(a.debug & 512)) {  // accumulator h of the previous tile drained (the epilogue
-              bar_wait(&t_empty[h], (i & 1) ^ 1);  // drains h = 0 first, so h = 0 MMAs overlap the h = 1 drain)
-              tc_fence_after();
+            const uint8_t* wt = w_s + sw * w_stage_bytes;
+            for (int h = 0; h < nh; ++h) {
+              if (ch == 0 && wh == 0) {  // accumulator h of the previous tile drained (the epilogue
+                bar_wait(&t_empty[h], (i & 1) ^ 1);  // drains h = 0 first, so h = 0 MMAs overlap the h = 1 drain)
+                tc_fence_after();
+              }
+              const int steps = (a.debug & 64) ? 0 : 4 / wsplit;
+              for (int jj = 0; jj < steps; ++jj) {
+                const int j = wh * (4 / wsplit) + jj;  // 16-element K step within the chunk
+                const uint64_t ad = sw128_desc(at) + 2 * j;  // +32 B per 16 K
+                const uint64_t bd = kc_w_desc(wt + h * (kUmmaN / 64) * wrows * 128 + jj * 2048, wrows * 128);
+                umma_i(tmem + h * kUmmaN, ad, bd, idesc, (ch > 0 || j > 0) ? 1u : 0u);
+              }
+              // last chunk: accumulator h is complete once its last MMAs are -- the epilogue can start
+              // draining it while the other accumulator's last MMAs run
+              if (ch == nch - 1 && wh == wsplit - 1) umma_commit(&t_full[h]);
             }
-#pragma unroll
-            for (int j = 0; j < ((a.debug & 64) ? 0 : 4); ++j) {
-              const uint64_t ad = sw128_desc(at) + 2 * j;                             // +32 B per 16 K
-              const uint64_t bd = kc_w_desc(wt + h * (kUmmaN / 64) * kKcWBox + j * 2048);  // 16 K rows per step
-              umma_i(tmem + h * kUmmaN, ad, bd, idesc, (ch > 0 || j > 0) ? 1u : 0u);
-            }
-            // last chunk: accumulator h is complete once these MMAs are -- the epilogue can start
-            // draining it while the other accumulator's last MMAs run
-            if (ch == nch - 1 && !(a.debug & 1024)) umma_commit(&t_full[h]);
+            umma_commit(&w_empty[sw]);
           }
           umma_commit(&a_empty[sa]);
-          umma_commit(&w_empty[sw]);
-          if (ch == nch - 1 && (a.debug & 1024))  // experiment: both accumulators committed after the unit
-            for (int h = 0; h < nh; ++h) umma_commit(&t_full[h]);
         }
       }
     }
@@ -1082,7 +1166,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
 }
 
 static size_t linear_kc_smem_bytes(int D) {
-  return 1024 + static_cast<size_t>(kKcWStages) * (D / 64) * kKcWBox + kKcAStages * kKcABytes +
+  (void)D;  // the layout is sized for D = 512 (z_s at a fixed offset)
+  return 1024 + static_cast<size_t>(kKcWStages) * (512 / 64) * kKcWBox + 4 * kKcABytes + 64 +
          kEpiWarps * kEpiBufs * kStageBytes + 256;
 }
 
@@ -1097,7 +1182,7 @@ bool encode_w_map_kc(const LinearArgs& a, CUtensorMap* m) {
   if (encode == nullptr) return false;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.F), static_cast<cuuint64_t>(a.H)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.D) * 2, static_cast<cuuint64_t>(a.F) * a.D * 2};
-  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kKcChunk), 1};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kKcChunk / 2), 1};  // one half chunk
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(m, a.out_dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                 const_cast<void*>(a.W), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1115,6 +1200,18 @@ bool encode_a_map_kc(const LinearArgs& a, CUtensorMap* m) {
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKcChunk), 1};
   const cuuint32_t estr[2] = {1, 1};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// fp32 records: {record element, row} of fp32, box 32 elements (128 B) x 1 row, 128-byte swizzle.
+bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (encode == nullptr) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.rec_stride / 4), static_cast<cuuint64_t>(a.shards[0].n_hbm)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.rec_stride)};
+  const cuuint32_t box[2] = {32, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1148,6 +1245,14 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
     a.tma_a = encode_a_map_kc(a, &amap) ? want_tma : 0;
+  // fp32 records: gather4 of 32-element halves into a staging ring, converted by four warps
+  // (PPLOAD_LINEAR_TMA_F32=0 keeps the register-staged producers)
+  const char* tf = getenv("PPLOAD_LINEAR_TMA_F32");
+  a.tma_f32 = 0;
+  if (!(tf && !strcmp(tf, "0")) && a.in_dtype == 0 && a.F % kKcChunk == 0 && a.world == 1 &&
+      a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
+      a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
+    a.tma_f32 = encode_a_map_f32_kc(a, &amap) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
   cfg.blockDim = dim3(kLinThreads);

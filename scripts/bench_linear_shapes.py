@@ -52,22 +52,43 @@ for name in os.environ.get("LIN_SHAPES", "igb_large,mag240m").split(","):
     with torch.cuda.stream(st):
         epoch(0)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3
-    with torch.cuda.stream(st):
-        a.record(st)
-        for r in range(reps):
-            epoch(1 + r)
-        b.record(st)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+
+    def timed(reps=3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            a.record(st)
+            for r in range(reps):
+                epoch(1 + r)
+            b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    # LIN_AB="d1,d2": interleaved A/B of PPLOAD_DEBUG_LINEAR values in this process (box-to-box clock
+    # and power differences would swamp a few per cent between separate runs)
+    ab = os.environ.get("LIN_AB")
+    if ab:
+        vals = ab.split(",")
+        res = {v: [] for v in vals}
+        for rnd in range(4):
+            for v in vals:
+                os.environ["PPLOAD_DEBUG_LINEAR"] = v
+                res[v].append(timed(2))
+        os.environ.pop("PPLOAD_DEBUG_LINEAR")
+        print(json.dumps({"shape": name, "ab_ms_per_epoch": {v: sorted(x) for v, x in res.items()},
+                          "ab_median_ms": {v: sorted(x)[len(x) // 2] for v, x in res.items()}}), flush=True)
+    import bench  # the NVML clock sampler of the bench line
+
+    clk = bench.ClockSampler(torch.cuda.current_device())
+    with clk:
+        ms = timed()
+    clocks = clk.summary()
     per_node = H * F * c["s_in"] + H * D * 2 + 4
     flops = 2.0 * H * F * D
     print(json.dumps({"shape": name, "debug": os.environ.get("PPLOAD_DEBUG_LINEAR", "0"), "rows": ROWS, "H": H, "F": F, "B": B, "D": D, "steps_per_launch": K,
                       "ms_per_epoch": ms, "nodes_per_s": ROWS / ms * 1e3, "hbm_bytes_per_node": per_node,
                       "achieved_GBs": ROWS * per_node / ms / 1e6, "frac_hbm": ROWS * per_node / ms / 1e6 / PEAK_HBM,
                       "tflops": ROWS * flops / ms / 1e9, "frac_tensor": ROWS * flops / ms / 1e9 / PEAK_TF,
-                      "w_l2_bytes_per_node": H * F * D * 2 / 128}), flush=True)
+                      "w_l2_bytes_per_node": H * F * D * 2 / 128, "clocks": clocks}), flush=True)
     L.close()
     del Z
     torch.cuda.empty_cache()

@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_linear_kc.py tests/test_gpu_linear.py -q -ra -x > gpurun_out/pytest_r2t.txt 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_r2t.txt
+rm -f gpurun_out/lin_r2t.jsonl
+for d in 0 64 16 1; do PPLOAD_DEBUG_LINEAR=$d timeout 600 python scripts/bench_linear_shapes.py >> gpurun_out/lin_r2t.jsonl 2>> gpurun_out/lin_shapes.err; done
+LIN_K=8 timeout 600 python scripts/bench_linear.py > gpurun_out/lin_products.jsonl 2>> gpurun_out/lin_shapes.err
+echo done

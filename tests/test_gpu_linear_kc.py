@@ -174,3 +174,20 @@ def test_kc_tma_gather4_sixteen_bit(pp, monkeypatch, tma_a, dt, F, chunk):
         L.epoch_permute(10, chunk)
         order = oracle.epoch_order(10, S.shape[0], chunk, node_set=S)
         run_and_check(pp, L, X, dt, hs, rs, H, F, D, order, B, dt, "f32", k=3)
+
+
+@pytest.mark.parametrize("tma_f32", ["1", "0"])
+@pytest.mark.parametrize("F,out_dt,chunk", [(128, oracle.BF16, 1), (192, oracle.F16, 33), (1024, oracle.BF16, 256)])
+def test_kc_tma_gather4_fp32_staging(pp, monkeypatch, tma_f32, F, out_dt, chunk):
+    # fp32 records with F % 64 == 0 in HBM: 32-element halves by TMA gather4 into the staging ring,
+    # cast by four converter warps (PPLOAD_LINEAR_TMA_F32=1, default) or the register producers (0)
+    monkeypatch.setenv("PPLOAD_LINEAR_TMA_F32", tma_f32)
+    monkeypatch.setenv("PPLOAD_LINEAR", "kc")
+    H, N, B, D = 2, 2300, 320, 512
+    X, hs, rs = hop_tensor(80 + F, H, N, F)
+    S = make_node_set(81, N, 1901)
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   node_set=S, batch_size=B, out_dtype=out_dt) as L:
+        L.epoch_permute(11, chunk)
+        order = oracle.epoch_order(11, S.shape[0], chunk, node_set=S)
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, out_dt, "f32", k=3)
