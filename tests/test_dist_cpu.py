@@ -30,7 +30,8 @@ def _worker(rank, world, port, q):
             mismatch_raised = False
         except ValueError:
             mismatch_raised = True
-        q.put((rank, ok_handles, mismatch_raised))
+        uid = ppd.broadcast_nccl_id(make_id=lambda: bytes(range(128)))  # plumbing only: a fake id
+        q.put((rank, ok_handles and uid == bytes(range(128)), mismatch_raised))
     finally:
         dist.destroy_process_group()
 
