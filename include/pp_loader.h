@@ -314,9 +314,14 @@ pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_str
  * PAPER.md:184-185) in one tensor-core kernel:
  *   Z[j, k, :] = bf16_rne(X_k[v_j, :]) @ W_k      (fp32 accumulation)
  * The batch itself is never written to memory.
- *   W: device bf16 [H][F][D] row-major (W_k = W[k] is F x D), 16-B aligned.
- *   D: 256 or 512.  Requires an fp32, HBM-resident (no spill) store with
- *      F <= 128, F % 4 == 0, and W == 1.
+ * X_k is the batch the loader would produce: fp32 records cast to the batch
+ * dtype (bf16 / f16, RNE), 16-bit records as they are.
+ *   W: device [H][F][D] row-major in the batch dtype (W_k = W[k] is F x D),
+ *      16-B aligned.
+ *   D: 256 or 512.  F % 4 == 0 for fp32 records, F % 8 == 0 for 16-bit ones;
+ *      any placement (HBM, spilled, sharded W > 1, compact store).  fp32 ->
+ *      bf16 HBM stores with F <= 128 and W == 1 take the W-resident kernel,
+ *      everything else the K-chunked one (PPLOAD_LINEAR=kc forces it).
  *   Z: device [n][B][H][D] of z_dtype (PP_BF16: RNE from fp32, or PP_F32),
  *      slot pitch z_stride_bytes (>= B*H*D*elem when n > 1), 16-B aligned.
  * W is read by TMA at every launch (nothing is cached across calls), so it may

@@ -123,10 +123,11 @@ struct LinearArgs {
   ShardView shards[kMaxWorld];
   int32_t tma_a = 0;                    // set by launch_gather_linear_kc: A chunks by TMA tile::gather4
   int32_t tma_f32 = 0;                  // set by launch_gather_linear_kc: fp32 records by gather4 into staging
+  int32_t pair = 0;                     // set by launch_gather_linear_kc: CTA pairs (cta_group::2, M = 256)
 };
 bool linear_supported(int H, int F, int D, int num_sms);
 // The K-chunked kernel: F % 8 == 0, D in {256, 512}, 16-bit batch dtype.
-bool linear_kc_supported(int H, int F, int D, int num_sms, int out_dtype);
+bool linear_kc_supported(int H, int F, int D, int num_sms, int in_dtype, int out_dtype);
 cudaError_t launch_gather_linear_kc(const LinearArgs& a, bool pdl, cudaStream_t st);
 // Encodes the Z and W tensor maps and launches the fused kernel on `st`.
 // pdl: programmatic dependent launch (only right after another fused launch of this

@@ -102,6 +102,16 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+__device__ __forceinline__ uint4 lds16(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ uint4 ldg16(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -664,8 +674,150 @@ __device__ __forceinline__ uint32_t f16x2(uint32_t lo, uint32_t hi) {
   const __half2 h = __floats2half2_rn(__uint_as_float(lo), __uint_as_float(hi));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+
+// ---- CTA-pair (cta_group::2) helpers: the leader (cluster rank 0) issues the M = 256 MMAs over both
+// CTAs' shared memory; the peer's producers and epilogue signal the leader's barriers remotely.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same object in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_addr(p)));
+  return r;
+}
+__device__ __forceinline__ void bar_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx_remote(uint32_t caddr, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(caddr), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait_cluster(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
+        "p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void umma_i2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the leader's MMAs so far complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+// Slot and phase of a counter walking a ring of n barrier-guarded slots -- no 64-bit division on the
+// single-lane issue paths (the MMA and TMA issuers are instruction-bound, not just barrier-bound).
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  int n;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ __forceinline__ void next() {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// MMA issue / commit for the K-chunked kernel.  kElect: executed by the whole (converged) warp, one
+// lane elected inside the instruction sequence -- the operands are warp-uniform, so they live in
+// uniform registers and no per-instruction waterfall loop is needed; otherwise by one lane.
+#define PPL_KC_MMA(CG, ELECT)                                                                         \
+  asm volatile("{\n .reg .pred e, p;\n" ELECT "setp.ne.b32 p, %4, 0;\n"                            \
+               " @e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d), \
+               "l"(a), "l"(b), "r"(idesc), "r"(accumulate)                                           \
+               : "memory")
+template <bool kPair, bool kElect>
+__device__ __forceinline__ void kc_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kPair && kElect)
+    PPL_KC_MMA("2", " elect.sync _|e, 0xffffffff;\n");
+  else if constexpr (kPair)
+    PPL_KC_MMA("2", " setp.eq.u32 e, 0, 0;\n");
+  else if constexpr (kElect)
+    PPL_KC_MMA("1", " elect.sync _|e, 0xffffffff;\n");
+  else
+    PPL_KC_MMA("1", " setp.eq.u32 e, 0, 0;\n");
+}
+#undef PPL_KC_MMA
+template <bool kPair, bool kElect>
+__device__ __forceinline__ void kc_commit(uint64_t* bar) {
+  if constexpr (kPair && kElect)
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e tcgen05.commit.cta_group::2.mbarrier::arrive::one"
+        ".shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(smem_addr(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+  else if constexpr (kPair)
+    umma_commit_pair(bar);
+  else if constexpr (kElect)
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e tcgen05.commit.cta_group::1.mbarrier::arrive::one"
+        ".shared::cluster.b64 [%0];\n}" ::"r"(smem_addr(bar))
+        : "memory");
+  else
+    umma_commit(bar);
+}
+
+// TMA loads whose completion goes to the leader's barrier in pair mode (.cta_group::2: the barrier
+// may sit in either CTA of the pair; the data lands in the issuing CTA's shared memory)
+template <bool kPair>
+__device__ __forceinline__ void tma_gather4(uint32_t dst, uint64_t map, int col, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+  if constexpr (kPair)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+template <bool kPair>
+__device__ __forceinline__ void tma_load3(uint32_t dst, uint64_t map, int c0, int c1, int c2, uint32_t bar) {
+  if constexpr (kPair)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
 }  // namespace
 
+// kPair: CTA pairs (clusters of 2, cta_group::2).  A pair takes 256-row tiles, each CTA gathering its
+// own 128 rows into its A stages and loading half of each accumulator's W columns (128 of 256); the
+// leader issues M = 256 x N = 256 MMAs that read both CTAs' shared memory, and each CTA's TMEM holds
+// its 128 rows of the accumulators.  Half the W bytes per row and per CTA stage, so twice the stages.
+template <bool kPair>
 __global__ void __launch_bounds__(kLinThreads, 1)
     k_gather_linear_kc(const LinearArgs a, const __grid_constant__ CUtensorMap zmap,
                        const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap) {
@@ -676,13 +828,15 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   // Default: whole-chunk W stages (2 x 64 KB at D = 512) and 4 slots (fp32 gathers: 2 A stages + 2
   // staging halves).  Experiment bit 2048: 3 half-chunk W stages + 6 slots (measured slower in
   // interleaved A/B runs: IGB-large rows 26 vs 20 ms, MAG240M rows 24 vs 16 ms, r2x).
-  const bool six = (a.debug & 2048) != 0;
+  const bool six = !kPair && (a.debug & 2048) != 0;
+  constexpr int npeer = kPair ? 2 : 1;
+  constexpr int bpa = kUmmaN / 64 / npeer;                // 64-column W blocks per accumulator in this CTA
   const int wsplit = six ? 2 : 1;                         // W stages per chunk
   const int wrows = kKcChunk / wsplit;                    // K rows per W stage
-  const int w_stage_bytes = (D / 64) * wrows * 128;
-  const int nws = six ? 3 : 2;                            // W stages
+  const int wbrows = six ? 32 : 64;                       // K rows per W TMA box (must match encode_w_map_kc)
+  const int w_stage_bytes = (D / npeer / 64) * wrows * 128;
+  const int nws = six ? 3 : 2 * npeer;                    // W stages
   const int nas = six ? 6 : 4;                            // A / staging slots
-  const int nstg = nas - 2;                               // fp32 staging halves (tma_f32)
   uint8_t* w_s = smem;                                    // [nws][D / 64 blocks][wrows K rows][128 B]
   uint8_t* a_s = w_s + nws * w_stage_bytes;               // [nas][128 rows][128 B]
   uint8_t* z_s = w_s + 4 * ((512 / 64) * kKcWBox) + 4 * kKcABytes;  // epilogue staging (fixed offset)
@@ -693,34 +847,62 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint64_t* w_empty = w_full + kKcWStages;                // [kKcWStages]
   uint64_t* t_full = w_empty + kKcWStages;                // [2]
   uint64_t* t_empty = t_full + 2;                         // [2]
-  uint64_t* stg_full = t_empty + 2;                       // [4] fp32 staging halves (tma_f32)
-  uint64_t* stg_empty = stg_full + 4;                     // [4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 4);
+  uint64_t* stg_full = t_empty + 2;                       // [kKcASlots] fp32 staging halves (tma_f32)
+  uint64_t* stg_empty = stg_full + kKcASlots;             // [kKcASlots]
+  uint64_t* fin = stg_empty + kKcASlots;                  // pair mode: the leader's MMAs all complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, F = a.F;
-  const int k = blockIdx.x % H;
-  const int q = blockIdx.x / H, Q = gridDim.x / H;
+  const uint32_t cr = kPair ? cluster_rank() : 0u;       // rank in the pair (0 = leader)
+  const int pid = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int k = pid % H;
+  const int q = pid / H, Q = (kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x)) / H;
+  constexpr int kTM = kTileM * npeer;                     // rows per tile (the pair's)
+  // barrier signals that go to the leader in pair mode
+  auto arrive_leader = [&](uint64_t* b) {
+    if constexpr (kPair)
+      bar_arrive_remote(leader_addr(b));
+    else
+      bar_arrive(b);
+  };
+  auto expect_leader = [&](uint64_t* b, uint32_t tx) {
+    if constexpr (kPair)
+      bar_expect_tx_remote(leader_addr(b), tx);
+    else
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
+  };
+  auto tma_bar = [&](uint64_t* b) -> uint32_t { return kPair ? leader_addr(b) : smem_addr(b); };
+  auto wait_leader = [&](uint64_t* b, uint32_t parity) {  // a barrier the peer CTA also signals
+    if constexpr (kPair)
+      bar_wait_cluster(b, parity);
+    else
+      bar_wait(b, parity);
+  };
   const int nh = D / kUmmaN;
   const int nch = (F + kKcChunk - 1) / kKcChunk;
+  // every W chunk of hop k fits the W stages (F <= 128; <= 256 for pairs): load W_k once and keep it
+  const bool wres = nch * (kKcChunk / (six ? 32 : 64)) <= (six ? 3 : 2 * npeer) && !six;
   const int s_in = a.in_dtype == 0 ? 4 : 2;
-  // A stages: 6 (16-bit TMA gathers), 4 (register producers), 2 (fp32 TMA gathers, whose slots 2-5
-  // hold four fp32 staging halves of 128 rows x 32 fp32, SW128)
-  const int na = a.tma_f32 ? 2 : nas;
-  uint8_t* stg = a_s + 2 * kKcABytes;
+  // A stages: one per slot (16-bit TMA gathers, register producers); fp32 TMA gathers use the slots in
+  // pairs: chunk u's two 32-element fp32 halves (128 rows x 128 B, SW128) land in slots 2p and 2p + 1
+  // (p = u mod nas / 2) and are converted in place -- the bf16 / f16 A chunk overwrites half 0 in slot
+  // 2p, which the MMA then reads; slot 2p + 1 is free again as soon as it is converted
+  const int na = a.tma_f32 ? nas / 2 : nas;
+  const int a_slot_step = a.tma_f32 ? 2 : 1;  // A chunk of ring position s at slot s * a_slot_step
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kKcASlots; ++s) {
       // arrivals: TMA gathers (16-bit) one arrive + the bytes; fp32 converters 128; register producers 256
-      bar_init(&a_full[s], a.tma_a ? 1 : a.tma_f32 ? 128 : kProducerThreads);
+      bar_init(&a_full[s], (a.tma_a ? 1 : a.tma_f32 ? 128 : kProducerThreads) * npeer);
       bar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < kKcASlots; ++s) {
       bar_init(&stg_full[s], 1);
       bar_init(&stg_empty[s], 128);
     }
     for (int s = 0; s < kKcWStages; ++s) {  // (only the first nws are used)
-      bar_init(&w_full[s], 1);
+      bar_init(&w_full[s], npeer);
       bar_init(&w_empty[s], 1);
     }
     for (int h = 0; h < 2; ++h) {
@@ -730,27 +912,43 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         const int lo = g * D / kEpiGroups, hi = (g + 1) * D / kEpiGroups;
         if (lo < (h + 1) * kUmmaN && hi > h * kUmmaN) cnt += 128;
       }
-      bar_init(&t_empty[h], cnt > 0 ? cnt : 1);
+      bar_init(&t_empty[h], cnt > 0 ? cnt * npeer : 1);
     }
+    bar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();  // the peer signals the leader's barriers: both initialised first
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t tiles_per_step = (a.B + kTileM - 1) / kTileM;
+  const int64_t tiles_per_step = (a.B + kTM - 1) / kTM;
   const int64_t total = tiles_per_step * a.nsteps;
   auto tile_rows = [&](int64_t t, int64_t& step, int& r0, int64_t& pos) -> int {
     step = t / tiles_per_step;
-    r0 = static_cast<int>(t - step * tiles_per_step) * kTileM;
+    r0 = static_cast<int>(t - step * tiles_per_step) * kTM;
     pos = a.first_pos + step * a.step_stride;
     const int64_t nrows = min(static_cast<int64_t>(a.B), a.N - pos);
-    return static_cast<int>(min(static_cast<int64_t>(kTileM), nrows - r0));
+    return static_cast<int>(min(static_cast<int64_t>(kTM), nrows - r0));
+  };
+  // this CTA's rows of tile t (its 128-row half in pair mode; may be empty for the peer)
+  auto tile_rows_cta = [&](int64_t t, int64_t& step, int& r0, int64_t& pos) -> int {
+    const int rows = tile_rows(t, step, r0, pos);
+    if constexpr (!kPair) return rows;
+    r0 += static_cast<int>(cr) * kTileM;
+    return max(0, min(kTileM, rows - static_cast<int>(cr) * kTileM));
   };
   auto next_tile = [&](int64_t t) -> int64_t {
     for (; t < total; t += Q) {
@@ -771,11 +969,11 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // their 8 gather4s; warp 0 also posts the stage's expected bytes.
     __shared__ int32_t s_rows[kTileM];
     const uint64_t amap_addr = reinterpret_cast<uint64_t>(&amap);
-    int64_t u = 0;
+    Ring ra(na);
     for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
       int64_t step, pos;
       int r0;
-      const int rows = tile_rows(t, step, r0, pos);
+      const int rows = tile_rows_cta(t, step, r0, pos);
       __syncwarp();
       for (int j = warp * (kTileM / gw) + lane; j < (warp + 1) * (kTileM / gw); j += 32) {
         int64_t v = 0;  // rows past the batch gather record 0; the epilogue never stores them
@@ -786,19 +984,21 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         s_rows[j] = static_cast<int32_t>(v);
       }
       __syncwarp();
-      for (int ch = 0; ch < nch; ++ch, ++u) {
-        if (a.tma_f32) {  // fp32 records: two 32-element halves into the staging slots, converted by warps 4-7
+      for (int ch = 0; ch < nch; ++ch) {
+        if (a.tma_f32) {  // fp32 records: two 32-element halves into slots 2p, 2p + 1, converted by warps 4-7
           if (lane == 0) {
+            const int p = ra.s;
+            bar_wait(&a_empty[p], ra.ph ^ 1u);               // slot 2p: the MMA is done with A(u - na)
+            bar_wait(&stg_empty[2 * p + 1], ra.ph ^ 1u);     // slot 2p + 1: converted
+            ra.next();
             for (int hh = 0; hh < 2; ++hh) {
-              const int64_t v = 2 * u + hh;  // staging half v in slot v % nstg
-              const int sl = static_cast<int>(v % nstg);
-              bar_wait(&stg_empty[sl], (static_cast<uint32_t>(v / nstg) & 1u) ^ 1u);
+              const int sl = 2 * p + hh;
               if (warp == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[sl])),
                              "r"(kKcABytes)
                              : "memory");
               const int col = k * F + ch * kKcChunk + hh * 32;
-              uint8_t* dst = stg + sl * kKcABytes;
+              uint8_t* dst = a_s + sl * kKcABytes;
               for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
                 asm volatile(
                     "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
@@ -811,57 +1011,66 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           continue;
         }
         if (lane == 0) {
-          const int s = static_cast<int>(u % na);
-          bar_wait(&a_empty[s], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
-          if (warp == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&a_full[s])),
-                         "r"(kKcABytes)
-                         : "memory");
+          const int s = ra.s;
+          bar_wait(&a_empty[s], ra.ph ^ 1u);
+          ra.next();
+          if (warp == 0) expect_leader(&a_full[s], kKcABytes);
           const int col = k * F + ch * kKcChunk;
           uint8_t* dst = a_s + s * kKcABytes;
+          const uint32_t fb = tma_bar(&a_full[s]);
           for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 512)),
-                "l"(amap_addr), "r"(col), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
-                "r"(s_rows[4 * g + 3]), "r"(smem_addr(&a_full[s]))
-                : "memory");
+            tma_gather4<kPair>(smem_addr(dst + g * 512), amap_addr, col, s_rows[4 * g], s_rows[4 * g + 1],
+                               s_rows[4 * g + 2], s_rows[4 * g + 3], fb);
         }
       }
     }
     __syncwarp();
   } else if (a.tma_f32 && warp < kProducerWarps) {
-    // ---------------- fp32 records gathered by TMA: warps 4-7 convert the staged halves (SW128 fp32,
-    // 32 per row) into the SW128 bf16 / f16 A chunk: thread (row r, 16-B A chunk j of the half) reads
-    // staged chunks 2j, 2j+1 (8 fp32), converts with cvt.rn, writes one 16-byte A chunk.
+    // ---------------- fp32 records gathered by TMA: warps 4-7 convert chunk u's staged halves (SW128
+    // fp32, 32 per row) into the SW128 bf16 / f16 A chunk in slot 2p, in place: thread (row r, 16-B A
+    // chunk j of the half) reads staged chunks 2j, 2j+1 (8 fp32), converts with cvt.rn, writes one
+    // 16-byte A chunk.  The four threads of a row are consecutive lanes of one warp, so a __syncwarp
+    // between the reads and the writes of half 0 orders every read of a row before the writes into it.
     const int tid = threadIdx.x - 128;
-    int64_t u = 0;
+    const uint32_t a_base = smem_addr(a_s);
+    Ring ra(na);
     for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
-      for (int ch = 0; ch < nch; ++ch, ++u) {
-        const int sa = static_cast<int>(u % na);
-        bar_wait(&a_empty[sa], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
-        uint8_t* at = a_s + sa * kKcABytes;
+      for (int ch = 0; ch < nch; ++ch, ra.next()) {
+        const int p = ra.s;
+        const uint32_t at = a_base + 2 * p * kKcABytes;
         for (int hh = 0; hh < 2; ++hh) {
-          const int64_t v = 2 * u + hh;
-          const int sl = static_cast<int>(v % nstg);
-          bar_wait(&stg_full[sl], static_cast<uint32_t>(v / nstg) & 1u);
-          const uint8_t* sh = stg + sl * kKcABytes;
+          const int sl = 2 * p + hh;
+          bar_wait(&stg_full[sl], ra.ph);
+          const uint32_t sh = a_base + sl * kKcABytes;
+          uint4 x[4][2];
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int item = tid + 128 * it;
             const int r = item >> 2, j = item & 3;
-            const uint4 x0 = *reinterpret_cast<const uint4*>(sh + r * 128 + (((2 * j) ^ (r & 7)) << 4));
-            const uint4 x1 = *reinterpret_cast<const uint4*>(sh + r * 128 + (((2 * j + 1) ^ (r & 7)) << 4));
+            x[it][0] = lds16(sh + r * 128 + (((2 * j) ^ (r & 7)) << 4));
+            x[it][1] = lds16(sh + r * 128 + (((2 * j + 1) ^ (r & 7)) << 4));
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int item = tid + 128 * it;
+            const int r = item >> 2, j = item & 3;
+            uint4 x0 = x[it][0], x1 = x[it][1];
+            // F % 64 != 0: elements past F belong to the next hop (or are the map's zero fill); the
+            // K padding must be zero (F % 4 == 0, so a 16-byte group is all in or all out)
+            const int e0 = ch * kKcChunk + hh * 32 + 8 * j;
+            if (e0 >= F) x0 = make_uint4(0, 0, 0, 0);
+            if (e0 + 4 >= F) x1 = make_uint4(0, 0, 0, 0);
             const uint4 y = a.out_dtype == 2
                                 ? make_uint4(f16x2(x0.x, x0.y), f16x2(x0.z, x0.w), f16x2(x1.x, x1.y), f16x2(x1.z, x1.w))
                                 : make_uint4(bf16x2(x0.x, x0.y), bf16x2(x0.z, x0.w), bf16x2(x1.x, x1.y),
                                              bf16x2(x1.z, x1.w));
-            *reinterpret_cast<uint4*>(at + sw128(r, hh * 4 + j)) = y;
+            sts16(at + sw128(r, hh * 4 + j), y);
           }
-          bar_arrive(&stg_empty[sl]);
+          if (hh == 1) bar_arrive(&stg_empty[sl]);  // slot 2p + 1 read out; slot 2p now holds A(u)
         }
         fence_async_smem();
-        bar_arrive(&a_full[sa]);
+        arrive_leader(&a_full[p]);
       }
     }
   } else if (a.tma_a && warp < kProducerWarps) {  // warps 4-7
@@ -878,7 +1087,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       if (t >= total) return kNoRow;
       int64_t step, pos;
       int r0;
-      const int rows = tile_rows(t, step, r0, pos);
+      const int rows = tile_rows_cta(t, step, r0, pos);
       uint32_t v = kNoRow;
       if (lane < 16 && rbase + lane < rows)
         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a.order + pos + r0 + rbase + lane));
@@ -918,9 +1127,11 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         }
       }
     };
-    auto store_chunk = [&](int64_t u, const uint4 (&x)[8]) {
-      const int s = static_cast<int>(u % na);
-      bar_wait(&a_empty[s], (static_cast<uint32_t>(u / na) & 1u) ^ 1u);
+    Ring ra(na);
+    auto store_chunk = [&](const uint4 (&x)[8]) {
+      const int s = ra.s;
+      bar_wait(&a_empty[s], ra.ph ^ 1u);
+      ra.next();
       uint8_t* at = a_s + s * kKcABytes;
       if (f32) {
 #pragma unroll
@@ -939,7 +1150,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         }
       }
       fence_async_smem();
-      bar_arrive(&a_full[s]);
+      arrive_leader(&a_full[s]);
     };
     // Register-staged loads keep only two chunks (64 KB per SM) in flight, less than HBM latency
     // needs, so each lane also pulls its row's chunk pf chunks ahead into L2 with one bulk prefetch
@@ -957,7 +1168,6 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // Register ring of R chunks: the loads of unit u + R - 1 are issued before unit u is converted
     // and stored, across tile boundaries.  R = 2 for fp32 records (8 x 16 B per lane and chunk),
     // R = 4 for 16-bit records (4 x 16 B): 64 registers of loads in flight either way.
-    int64_t u = 0;  // unit counter: (tile, chunk) pairs in order
     int64_t lt = next_tile(q);  // the load cursor: tile, chunk, this lane's row pointer
     int lch = 0;
     const uint8_t* lsrc = lt < total ? resolve(fetch_index(lt)) : nullptr;
@@ -997,7 +1207,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
             }
           }
           if (!have[j]) return;
-          store_chunk(u++, x[j]);
+          store_chunk(x[j]);
         }
       }
     };
@@ -1009,71 +1219,84 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // ---------------- W loader: the same (tile, chunk) sequence; chunk ch of W_k into stage u % 2
     if (lane == 0) {
       const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
-      const uint32_t nbox = static_cast<uint32_t>(D / 64);
-      int64_t wv = 0;  // W stage-fill counter: (tile, chunk, part) in order
+      const uint32_t nbox = static_cast<uint32_t>(D / npeer / 64);
+      Ring rw(nws);  // W stage fills: (tile, chunk, part) in order
       for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
         for (int ch = 0; ch < nch; ++ch) {
-          for (int wh = 0; wh < wsplit; ++wh, ++wv) {
-            const int s = static_cast<int>(wv % nws);
-            bar_wait(&w_empty[s], (static_cast<uint32_t>(wv / nws) & 1u) ^ 1u);
+          for (int wh = 0; wh < wsplit; ++wh, rw.next()) {
+            const int s = rw.s;
+            bar_wait(&w_empty[s], rw.ph ^ 1u);
             if (a.debug & 16) {  // experiment: no W traffic (the MMAs read stale shared memory)
-              bar_arrive(&w_full[s]);
+              arrive_leader(&w_full[s]);
               continue;
             }
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&w_full[s])),
-                         "r"(w_stage_bytes)
-                         : "memory");
-            for (uint32_t b = 0; b < nbox; ++b)
-              for (int sub = 0; sub < wrows / 32; ++sub)  // 32-row boxes stacked inside the 64-column block
-                asm volatile(
-                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-                    "%4}], [%5];" ::"r"(smem_addr(w_s + s * w_stage_bytes + b * wrows * 128 + sub * kKcWBox)),
-                    "l"(wmap_addr), "r"(static_cast<int>(b * 64)), "r"(ch * kKcChunk + wh * wrows + sub * 32), "r"(k),
-                    "r"(smem_addr(&w_full[s]))
-                    : "memory");
+            expect_leader(&w_full[s], w_stage_bytes);
+            const uint32_t fb = tma_bar(&w_full[s]);
+            for (uint32_t b = 0; b < nbox; ++b) {
+              // block b: columns of accumulator b / bpa; in pair mode this CTA's half of them
+              const int col = static_cast<int>(b / bpa) * kUmmaN + static_cast<int>(cr) * (kUmmaN / 2) +
+                              static_cast<int>(b % bpa) * 64;
+              for (int sub = 0; sub < wrows / wbrows; ++sub)  // boxes stacked inside the 64-column block
+                tma_load3<kPair>(smem_addr(w_s + s * w_stage_bytes + b * wrows * 128 + sub * wbrows * 128), wmap_addr,
+                                 col, ch * kKcChunk + wh * wrows + sub * wbrows, k, fb);
+            }
           }
         }
+        if (wres) break;  // W_k resident in stages 0 .. nch - 1 for every tile
       }
     }
     __syncwarp();
   } else if (warp == kMmaWarp) {
-    // ---------------- MMA issuer: per unit, 4 K-steps of 16 into each accumulator
-    if (lane == 0) {
-      const uint32_t idesc = kc_idesc(a.out_dtype);
-      int64_t u = 0, wv = 0;
+    // ---------------- MMA issuer: per unit, 4 K-steps of 16 into each accumulator.  The whole warp runs
+    // the loop and one elected lane issues (experiment bit 16384: lane 0 alone runs it); in pair mode
+    // the leader issues for both CTAs.
+    auto mma_role = [&](auto warpwide) {
+      constexpr bool kW = decltype(warpwide)::value;
+      const uint32_t idesc =
+          kPair ? ((kc_idesc(a.out_dtype) & ~(0x1Fu << 24)) | (static_cast<uint32_t>(kTM >> 4) << 24)) : kc_idesc(a.out_dtype);
+      Ring ra(na), rw(nws);
       int i = 0;
       for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
-        for (int ch = 0; ch < nch; ++ch, ++u) {
-          const int sa = static_cast<int>(u % na);
-          bar_wait(&a_full[sa], static_cast<uint32_t>(u / na) & 1u);
+        for (int ch = 0; ch < nch; ++ch, ra.next()) {
+          const int sa = ra.s;
+          wait_leader(&a_full[sa], ra.ph);
           tc_fence_after();
-          const uint8_t* at = a_s + sa * kKcABytes;
+          const uint8_t* at = a_s + sa * a_slot_step * kKcABytes;
           // the chunk's W in wsplit stages (whole, or K rows 0-31 and 32-63)
-          for (int wh = 0; wh < wsplit; ++wh, ++wv) {
-            const int sw = static_cast<int>(wv % nws);
-            bar_wait(&w_full[sw], static_cast<uint32_t>(wv / nws) & 1u);
+          for (int wh = 0; wh < wsplit; ++wh, rw.next()) {
+            const int sw = wres ? ch : rw.s;
+            wait_leader(&w_full[sw], wres ? 0u : rw.ph);
             tc_fence_after();
             const uint8_t* wt = w_s + sw * w_stage_bytes;
             for (int h = 0; h < nh; ++h) {
               if (ch == 0 && wh == 0) {  // accumulator h of the previous tile drained (the epilogue
-                bar_wait(&t_empty[h], (i & 1) ^ 1);  // drains h = 0 first, so h = 0 MMAs overlap the h = 1 drain)
+                wait_leader(&t_empty[h], (i & 1) ^ 1);  // drains h = 0 first, so h = 0 MMAs overlap the h = 1 drain)
                 tc_fence_after();
               }
               const int steps = (a.debug & 64) ? 0 : 4 / wsplit;
-              for (int jj = 0; jj < steps; ++jj) {
-                const int j = wh * (4 / wsplit) + jj;  // 16-element K step within the chunk
-                const uint64_t ad = sw128_desc(at) + 2 * j;  // +32 B per 16 K
-                const uint64_t bd = kc_w_desc(wt + h * (kUmmaN / 64) * wrows * 128 + jj * 2048, wrows * 128);
-                umma_i(tmem + h * kUmmaN, ad, bd, idesc, (ch > 0 || j > 0) ? 1u : 0u);
-              }
+              // descriptors of the first K step; each further step of 16 advances A by 32 B and B by
+              // 16 K rows (2 KB) -- added to the start-address field (bits 0-13, 16-B units)
+              const uint64_t ad0 = sw128_desc(at) + 2 * (wh * (4 / wsplit));
+              const uint64_t bd0 = kc_w_desc(wt + h * bpa * wrows * 128, wrows * 128);
+              for (int jj = 0; jj < steps; ++jj)
+                kc_mma<kPair, kW>(tmem + h * kUmmaN, ad0 + 2 * jj, bd0 + 128 * jj, idesc,
+                                  (ch > 0 || wh > 0 || jj > 0) ? 1u : 0u);
               // last chunk: accumulator h is complete once its last MMAs are -- the epilogue can start
               // draining it while the other accumulator's last MMAs run
-              if (ch == nch - 1 && wh == wsplit - 1) umma_commit(&t_full[h]);
+              if (ch == nch - 1 && wh == wsplit - 1) kc_commit<kPair, kW>(&t_full[h]);
             }
-            umma_commit(&w_empty[sw]);
+            if (!wres) kc_commit<kPair, kW>(&w_empty[sw]);
           }
-          umma_commit(&a_empty[sa]);
+          kc_commit<kPair, kW>(&a_empty[sa]);
         }
+      }
+      if constexpr (kPair) kc_commit<kPair, kW>(fin);  // both CTAs learn when every MMA (and signal) landed
+    };
+    if (cr == 0) {
+      if (a.debug & 16384) {
+        if (lane == 0) mma_role(std::false_type{});
+      } else {
+        mma_role(std::true_type{});
       }
     }
     __syncwarp();
@@ -1088,7 +1311,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
       int64_t step, pos;
       int r0;
-      const int rows = tile_rows(t, step, r0, pos);
+      const int rows = tile_rows_cta(t, step, r0, pos);
       const bool tma_rows = a.z_tma && e * 32 + 32 <= rows;
       for (int h = 0; h < nh; ++h) {
         const int c_lo = max(grp * D / kEpiGroups, h * kUmmaN) - h * kUmmaN;
@@ -1152,16 +1375,30 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           }
         }
         tc_fence_before();
-        bar_arrive(&t_empty[h]);
+        arrive_leader(&t_empty[h]);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if constexpr (kPair) {
+    // no CTA leaves while the leader's MMAs may still read the peer's shared memory or signal its barriers
+    if (warp == kMmaWarp) {
+      if (lane == 0) bar_wait(fin, 0);
+      __syncwarp();
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == kMmaWarp) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+  } else {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
   }
 }
 
@@ -1171,8 +1408,8 @@ static size_t linear_kc_smem_bytes(int D) {
          kEpiWarps * kEpiBufs * kStageBytes + 256;
 }
 
-bool linear_kc_supported(int H, int F, int D, int num_sms, int out_dtype) {
-  return F >= 8 && F % 8 == 0 && (D == 256 || D == 512) && H >= 1 && H <= num_sms && (out_dtype == 1 || out_dtype == 2);
+bool linear_kc_supported(int H, int F, int D, int num_sms, int in_dtype, int out_dtype) {
+  return F >= 4 && F % (in_dtype == 0 ? 4 : 8) == 0 && (D == 256 || D == 512) && H >= 1 && H <= num_sms && (out_dtype == 1 || out_dtype == 2);
 }
 
 namespace {
@@ -1182,7 +1419,8 @@ bool encode_w_map_kc(const LinearArgs& a, CUtensorMap* m) {
   if (encode == nullptr) return false;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.D), static_cast<cuuint64_t>(a.F), static_cast<cuuint64_t>(a.H)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.D) * 2, static_cast<cuuint64_t>(a.F) * a.D * 2};
-  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kKcChunk / 2), 1};  // one half chunk
+  // one whole chunk per box (64 K rows), half a chunk in the half-chunk experiment layout (bit 2048)
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>((a.debug & 2048) ? kKcChunk / 2 : kKcChunk), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(m, a.out_dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                 const_cast<void*>(a.W), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1218,12 +1456,16 @@ bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m) {
 }  // namespace
 
 cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream_t st) {
-  if (!linear_kc_supported(a_in.H, a_in.F, a_in.D, a_in.num_sms, a_in.out_dtype)) return cudaErrorInvalidValue;
+  if (!linear_kc_supported(a_in.H, a_in.F, a_in.D, a_in.num_sms, a_in.in_dtype, a_in.out_dtype))
+    return cudaErrorInvalidValue;
   const size_t smem = linear_kc_smem_bytes(a_in.D);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gather_linear_kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_gather_linear_kc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(linear_kc_smem_bytes(512)));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gather_linear_kc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(linear_kc_smem_bytes(512)));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1249,21 +1491,34 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   // (PPLOAD_LINEAR_TMA_F32=0 keeps the register-staged producers)
   const char* tf = getenv("PPLOAD_LINEAR_TMA_F32");
   a.tma_f32 = 0;
-  if (!(tf && !strcmp(tf, "0")) && a.in_dtype == 0 && a.F % kKcChunk == 0 && a.world == 1 &&
+  if (!(tf && !strcmp(tf, "0")) && a.in_dtype == 0 && a.F % 4 == 0 && a.world == 1 &&
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
     a.tma_f32 = encode_a_map_f32_kc(a, &amap) ? 1 : 0;
+  // CTA pairs (cta_group::2, M = 256), opt-in with PPLOAD_LINEAR_PAIR=1: measured slower than
+  // single CTAs at every row shape (interleaved A/B, r2z*); experiment bit 8192 flips the choice
+  const char* pe = getenv("PPLOAD_LINEAR_PAIR");
+  bool pair = pe && !strcmp(pe, "1");
+  if (a.debug & 8192) pair = !pair;
+  pair = pair && (a.num_sms / 2) >= a.H && (a.debug & 2048) == 0;
+  a.pair = pair ? 1 : 0;
+  const int per = a.H * (pair ? 2 : 1);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((a.num_sms / a.H) * a.H);
+  cfg.gridDim = dim3((a.num_sms / per) * per);
   cfg.blockDim = dim3(kLinThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute lattr[1];
+  cudaLaunchAttribute lattr[2];
   lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   lattr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  lattr[1].id = cudaLaunchAttributeClusterDimension;
+  lattr[1].val.clusterDim.x = pair ? 2 : 1;
+  lattr[1].val.clusterDim.y = 1;
+  lattr[1].val.clusterDim.z = 1;
   cfg.attrs = lattr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gather_linear_kc, a, zmap, wmap, amap);
+  cfg.numAttrs = 2;
+  return pair ? cudaLaunchKernelEx(&cfg, k_gather_linear_kc<true>, a, zmap, wmap, amap)
+              : cudaLaunchKernelEx(&cfg, k_gather_linear_kc<false>, a, zmap, wmap, amap);
 }
 
 }  // namespace ppl

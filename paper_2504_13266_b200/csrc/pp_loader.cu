@@ -1439,8 +1439,8 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   const char* kc_env = getenv("PPLOAD_LINEAR");
   const bool resident = L->in_dtype == PP_F32 && L->out_dtype == PP_BF16 && L->n_spill == 0 && L->W == 1 &&
                         linear_supported(L->H, L->F, D, L->num_sms) && !(kc_env && !strcmp(kc_env, "kc"));
-  if (!resident && !linear_kc_supported(L->H, L->F, D, L->num_sms, L->out_dtype))
-    return fail(PP_ERR_INVALID, "fused linear supports F %% 8 == 0 (F %% 4 == 0 when F <= 128) and D in {256, 512} "
+  if (!resident && !linear_kc_supported(L->H, L->F, D, L->num_sms, L->in_dtype, L->out_dtype))
+    return fail(PP_ERR_INVALID, "fused linear supports F %% 4 == 0 (fp32 records) or F %% 8 == 0 (16-bit records) and D in {256, 512} "
                 "(F=%d, D=%d)", L->F, D);
   if (z_dtype != PP_BF16 && z_dtype != PP_F32) return fail(PP_ERR_INVALID, "z_dtype must be PP_BF16 or PP_F32");
   if (reinterpret_cast<uintptr_t>(W) % 16 || reinterpret_cast<uintptr_t>(Z) % 16 || z_stride_bytes % 16)

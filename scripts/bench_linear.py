@@ -71,12 +71,22 @@ def timeit(fn, reps=5):
     return a.elapsed_time(b) / reps
 
 
-for name, fn, bytes_per_row in (("fused_tcgen05", fused_epoch, H * F * 4 + H * D * 2 + 4),
-                                ("unfused_gather_then_cublas", unfused_epoch,
-                                 H * F * 4 + H * F * 2 + 4 + H * F * 2 + H * D * 2)):
-    ms = timeit(fn)
+# variants timed in interleaved rounds (box-to-box and power-state drift hits all alike); the
+# fused kernel is the W-resident one by default, PPLOAD_LINEAR=kc forces the K-chunked one
+VARIANTS = [("fused_tcgen05", fused_epoch, "", H * F * 4 + H * D * 2 + 4),
+            ("fused_tcgen05_kc", fused_epoch, "kc", H * F * 4 + H * D * 2 + 4),
+            ("unfused_gather_then_cublas", unfused_epoch, "", H * F * 4 + H * F * 2 + 4 + H * F * 2 + H * D * 2)]
+times = {v[0]: [] for v in VARIANTS}
+for rnd in range(int(os.environ.get("LIN_ROUNDS", "3"))):
+    for name, fn, mode, _ in VARIANTS:
+        os.environ["PPLOAD_LINEAR"] = mode
+        times[name].append(timeit(fn))
+os.environ.pop("PPLOAD_LINEAR", None)
+for name, fn, mode, bytes_per_row in VARIANTS:
+    ms = float(np.median(times[name]))
     flops = 2.0 * N * H * F * D
-    print(json.dumps({"variant": name, "steps_per_launch": K, "ms_per_epoch": ms, "nodes_per_s": N / ms * 1e3,
+    print(json.dumps({"variant": name, "steps_per_launch": K, "ms_per_epoch": ms, "rounds_ms": times[name],
+                      "nodes_per_s": N / ms * 1e3,
                       "hbm_bytes_per_row": bytes_per_row, "achieved_GBs": N * bytes_per_row / ms / 1e6,
                       "frac_hbm": N * bytes_per_row / ms / 1e6 / PEAK_HBM,
                       "tflops": flops / ms / 1e9, "frac_tensor": flops / ms / 1e9 / PEAK_TF}), flush=True)

@@ -71,8 +71,22 @@ for name in os.environ.get("LIN_SHAPES", "igb_large,mag240m").split(","):
         res = {v: [] for v in vals}
         for rnd in range(4):
             for v in vals:
-                os.environ["PPLOAD_DEBUG_LINEAR"] = v
+                # a token is a PPLOAD_DEBUG_LINEAR value, or "E:NAME=VAL+NAME2=VAL2" (environment settings)
+                saved = {}
+                if v.startswith("E:"):
+                    os.environ["PPLOAD_DEBUG_LINEAR"] = "0"
+                    for kv in v[2:].split("+"):
+                        key, val = kv.split("=", 1)
+                        saved[key] = os.environ.get(key)
+                        os.environ[key] = val
+                else:
+                    os.environ["PPLOAD_DEBUG_LINEAR"] = v
                 res[v].append(timed(2))
+                for key, old in saved.items():
+                    if old is None:
+                        os.environ.pop(key, None)
+                    else:
+                        os.environ[key] = old
         os.environ.pop("PPLOAD_DEBUG_LINEAR")
         print(json.dumps({"shape": name, "ab_ms_per_epoch": {v: sorted(x) for v, x in res.items()},
                           "ab_median_ms": {v: sorted(x)[len(x) // 2] for v, x in res.items()}}), flush=True)

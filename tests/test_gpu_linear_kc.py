@@ -43,9 +43,11 @@ def check(Zgpu, zdt, batch_bits, wbits, dt, F):
         tol = tol + 2.0 ** -8 * np.abs(Zref)
     else:
         got = Zgpu.cpu().numpy().astype(np.float64)
+    fin = np.isfinite(Zref)
     err = np.abs(got - Zref)
-    bad = err > tol
-    assert not bad.any(), f"{bad.sum()} of {bad.size} outside tolerance; worst excess {(err - tol).max()}"
+    bad = fin & ~(err <= tol)  # a NaN where the reference is finite fails too
+    assert not bad.any(), f"{bad.sum()} of {bad.size} outside tolerance; worst excess {np.nanmax(err[fin] - tol[fin])}"
+    assert not np.isfinite(got[~fin]).any(), "finite output where the reference overflows or is NaN"
 
 
 def run_and_check(pp, L, bits, in_dt, hs, rs, H, F, D, order, B, out_dt, zdt, W=1, r=0, k=2, seed=70):
@@ -191,3 +193,54 @@ def test_kc_tma_gather4_fp32_staging(pp, monkeypatch, tma_f32, F, out_dt, chunk)
         L.epoch_permute(11, chunk)
         order = oracle.epoch_order(11, S.shape[0], chunk, node_set=S)
         run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, out_dt, "f32", k=3)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("H,F,dt,D,B,path", [
+    (3, 256, oracle.F32, 512, 300, "tma"),      # fp32 gather4 + converters; tiles whose peer half is empty
+    (2, 768, oracle.F16, 512, 1000, "tma"),     # 16-bit gather4 straight into A
+    (4, 200, oracle.F32, 256, 640, "regs"),     # register producers (F % 64 != 0), one accumulator
+    (1, 128, oracle.BF16, 512, 4096, "regs"),   # many tiles per pair: both barrier parities, deep W ring
+    (80, 64, oracle.F16, 512, 256, "tma"),      # H > 148 / 2: single CTAs whatever the setting
+])
+def test_kc_cta_pair(pp, monkeypatch, pair, H, F, dt, D, B, path):
+    # CTA pairs (PPLOAD_LINEAR_PAIR=1, default): clusters of two, the leader issuing M = 256
+    # tcgen05.mma.cta_group::2 over both CTAs' A stages and W halves; each CTA drains its own rows
+    monkeypatch.setenv("PPLOAD_LINEAR_PAIR", pair)
+    monkeypatch.setenv("PPLOAD_LINEAR", "kc")
+    if path == "regs":
+        monkeypatch.setenv("PPLOAD_LINEAR_TMA_A", "0")
+        monkeypatch.setenv("PPLOAD_LINEAR_TMA_F32", "0")
+    N = 700 if H >= 80 else 5003
+    X, hs, rs = hop_tensor(100 + H + F, H, N, F, dtype=np.float32 if dt == oracle.F32 else np.uint16)
+    out_dt = oracle.BF16 if dt == oracle.F32 else dt
+    pdt = {oracle.F32: pp.PP_F32, oracle.F16: pp.PP_F16, oracle.BF16: pp.PP_BF16}[dt]
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pdt,
+                   batch_size=B, out_dtype=out_dt) as L:
+        L.epoch_permute(13, 1)
+        order = oracle.epoch_order(13, N, 1)
+        bits = X.view(np.uint32) if dt == oracle.F32 else X
+        zdt = "bf16" if D == 512 else "f32"
+        run_and_check(pp, L, bits, dt, hs, rs, H, F, D, order, B, out_dt, zdt, k=3)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("tma_f32", ["1", "0"])
+@pytest.mark.parametrize("F", [100, 36, 196])
+def test_kc_fp32_f_not_multiple_of_64(pp, monkeypatch, pair, tma_f32, F):
+    # fp32 records with F % 64 != 0 (products F = 100; F % 8 != 0 too): the last K chunk is padded
+    # with zeros -- the fp32 gather4 reads 32-element halves that run into the next hop, which the
+    # converters must zero (Inf planted at the start of hop 1 would otherwise poison hop 0's sums:
+    # 0 * Inf = NaN); F <= 128 keeps W_k resident in the W stages (<= 256 for pairs)
+    monkeypatch.setenv("PPLOAD_LINEAR", "kc")
+    monkeypatch.setenv("PPLOAD_LINEAR_PAIR", pair)
+    monkeypatch.setenv("PPLOAD_LINEAR_TMA_F32", tma_f32)
+    H, N, B, D = 3, 3001, 640, 512
+    X, hs, rs = hop_tensor(120 + F, H, N, F)
+    trap = np.random.default_rng(121).choice(N, 64, replace=False)
+    X[1, trap, :4] = np.inf
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(14, 1)
+        order = oracle.epoch_order(14, N, 1)
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "bf16", k=3)
