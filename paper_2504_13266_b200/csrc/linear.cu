@@ -759,6 +759,31 @@ __device__ __forceinline__ void kc_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
     PPL_KC_MMA("1", " setp.eq.u32 e, 0, 0;\n");
 }
 #undef PPL_KC_MMA
+// The four K = 16 steps of one 64-element chunk into one accumulator in one asm block, one lane
+// elected: A advances 32 B (+2 in the descriptor's 16-byte address field) and B 16 K rows (2 KB,
+// +128) per step; only the first step may start a fresh accumulation.
+#define PPL_KC_MMA4(CG)                                                                                 \
+  asm volatile(                                                                                         \
+      "{\n .reg .pred e, p;\n .reg .b64 a1, a2, a3, b1, b2, b3;\n"                                       \
+      " elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"                                          \
+      " add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"                                 \
+      " add.s64 b1, %2, 128;\n add.s64 b2, %2, 256;\n add.s64 b3, %2, 384;\n"                           \
+      " @e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], %1, %2, %3, p;\n"                               \
+      " @e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], a1, b1, %3, 1;\n"                               \
+      " @e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], a2, b2, %3, 1;\n"                               \
+      " @e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], a3, b3, %3, 1;\n}" ::"r"(tmem_d),                \
+      "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate)                                                     \
+      : "memory")
+template <bool kPair>
+__device__ __forceinline__ void kc_mma4(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                        uint32_t accumulate) {
+  if constexpr (kPair)
+    PPL_KC_MMA4("2");
+  else
+    PPL_KC_MMA4("1");
+}
+#undef PPL_KC_MMA4
+
 template <bool kPair, bool kElect>
 __device__ __forceinline__ void kc_commit(uint64_t* bar) {
   if constexpr (kPair && kElect)
@@ -1278,9 +1303,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
               // 16 K rows (2 KB) -- added to the start-address field (bits 0-13, 16-B units)
               const uint64_t ad0 = sw128_desc(at) + 2 * (wh * (4 / wsplit));
               const uint64_t bd0 = kc_w_desc(wt + h * bpa * wrows * 128, wrows * 128);
-              for (int jj = 0; jj < steps; ++jj)
-                kc_mma<kPair, kW>(tmem + h * kUmmaN, ad0 + 2 * jj, bd0 + 128 * jj, idesc,
-                                  (ch > 0 || wh > 0 || jj > 0) ? 1u : 0u);
+              if (kW && steps == 4 && !(a.debug & 32768)) {  // a whole chunk: one issue block
+                kc_mma4<kPair>(tmem + h * kUmmaN, ad0, bd0, idesc, (ch > 0 || wh > 0) ? 1u : 0u);
+              } else {
+                for (int jj = 0; jj < steps; ++jj)
+                  kc_mma<kPair, kW>(tmem + h * kUmmaN, ad0 + 2 * jj, bd0 + 128 * jj, idesc,
+                                    (ch > 0 || wh > 0 || jj > 0) ? 1u : 0u);
+              }
               // last chunk: accumulator h is complete once its last MMAs are -- the epilogue can start
               // draining it while the other accumulator's last MMAs run
               if (ch == nch - 1 && wh == wsplit - 1) kc_commit<kPair, kW>(&t_full[h]);

@@ -13,6 +13,9 @@ import re
 import subprocess
 import sys
 
+SRC = "paper_2504_13266_b200/csrc/linear.cu"
+SRC_NAME = "/" + SRC.rsplit("/", 1)[-1]
+
 
 def sass_lines(cubin, fn, min_line=0):
     """offset -> (source line, instruction).  The line is the outermost frame of the inlining chain,
@@ -30,7 +33,9 @@ def sass_lines(cubin, fn, min_line=0):
         if m:
             if fresh:
                 chain, fresh = [], False
-            chain.append(int(m.group(2)))  # innermost first, outermost last
+            # innermost first, outermost last; frames in other files (CUDA headers) are skipped
+            if m.group(1).endswith(SRC_NAME):
+                chain.append(int(m.group(2)))
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*)", ln)
         if m:
@@ -67,7 +72,7 @@ def main():
         for i, n in reasons:
             why[line][n] += int(r[i] or 0)
     tot = sum(per.values())
-    src = open("paper_2504_13266_b200/csrc/linear.cu").read().splitlines()
+    src = open(SRC).read().splitlines()
     print(f"# {rep}: {tot} samples")
     for line, s in per.most_common(top):
         text = src[line - 1].strip()[:90] if 0 < line <= len(src) else ""
