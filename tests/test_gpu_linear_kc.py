@@ -244,3 +244,43 @@ def test_kc_fp32_f_not_multiple_of_64(pp, monkeypatch, pair, tma_f32, F):
         L.epoch_permute(14, 1)
         order = oracle.epoch_order(14, N, 1)
         run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "bf16", k=3)
+
+
+@pytest.mark.parametrize("dt,F", [(oracle.F32, 256), (oracle.F32, 100), (oracle.F16, 192)])
+def test_kc_half_chunk_experiment_layout(pp, monkeypatch, dt, F):
+    # experiment bit 2048 (three half-chunk W stages, six A slots: three in-place fp32 slot pairs)
+    # must stay exact even though it is not the default
+    monkeypatch.setenv("PPLOAD_LINEAR", "kc")
+    monkeypatch.setenv("PPLOAD_DEBUG_LINEAR", "2048")
+    H, N, B, D = 2, 2600, 512, 512
+    X, hs, rs = hop_tensor(130 + F, H, N, F, dtype=np.float32 if dt == oracle.F32 else np.uint16)
+    out_dt = oracle.BF16 if dt == oracle.F32 else dt
+    pdt = pp.PP_F32 if dt == oracle.F32 else pp.PP_F16
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pdt,
+                   batch_size=B, out_dtype=out_dt) as L:
+        L.epoch_permute(15, 7)
+        order = oracle.epoch_order(15, N, 7)
+        bits = X.view(np.uint32) if dt == oracle.F32 else X
+        run_and_check(pp, L, bits, dt, hs, rs, H, F, D, order, B, out_dt, "bf16", k=3)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_kc_cta_pair_sharded_loopback(pp, monkeypatch, W):
+    # CTA pairs over a sharded store (register producers resolving owner / local row per row)
+    monkeypatch.setenv("PPLOAD_LINEAR_PAIR", "1")
+    H, N, F, B, D = 3, 4001, 128, 384, 512
+    X, hs, rs = hop_tensor(140 + W, H, N, F)
+    Ls = [pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                    batch_size=B, out_dtype=pp.PP_BF16, world_size=W, rank=r, peers=pp.PP_PEERS_LOOPBACK)
+          for r in range(W)]
+    pp.pp_link_loopback([L.h for L in Ls])
+    try:
+        order = oracle.epoch_order(16, N, 1)
+        for L in Ls:
+            L.epoch_permute(16, 1)
+        for r, L in enumerate(Ls):
+            run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "bf16",
+                          W=W, r=r, k=2)
+    finally:
+        for L in Ls:
+            L.close()
