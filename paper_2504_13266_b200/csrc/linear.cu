@@ -630,14 +630,16 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, bool pdl, cudaStream_t 
 }
 
 
-// ==== K-chunked variant: any F (% 8), 16-bit batch dtype, spilled / sharded stores ==============
+// ==== K-chunked variant: any F (% 4 fp32, % 8 16-bit), spilled / sharded stores ================
 // The F <= 128 kernel above keeps all of W_k resident; with F = 768 (MAG240M) or 1024 (IGB-large)
 // W_k is 0.75-1 MB, so here the reduction dimension is walked in chunks of 64: per 128-row M-tile
-// and chunk, the producers write a 16 KB A chunk (128 rows x 64 elements, K-major SWIZZLE_128B) and
-// a loader warp brings the matching 64 x D slice of W_k by TMA (D / 64 boxes of 64 x 64, MN-major
-// SWIZZLE_128B; rows >= F zero-filled).  4 A stages, 2 W stages, the same TMEM accumulators and
-// TMA-store epilogue as above.  W_k is re-read from L2 for every tile (it is the same for all of a
-// CTA's tiles), F x D x 2 bytes per 128 rows.
+// and chunk, a 16 KB A chunk (128 rows x 64 elements, K-major SWIZZLE_128B) is filled -- by TMA
+// tile::gather4 straight from the store (16-bit records), by gather4 of fp32 halves converted in
+// place (fp32 records), or by register-staged producers (spilled / sharded stores) -- and a loader
+// warp brings the matching 64 x D slice of W_k by TMA (D / 64 boxes of 64 x 64, MN-major
+// SWIZZLE_128B; rows >= F zero-filled).  2 W stages (W_k kept resident when it fits them), the same
+// TMEM accumulators and TMA-store epilogue as above.  Otherwise W_k is re-read from L2 for every
+// tile (it is the same for all of a CTA's tiles), F x D x 2 bytes per 128 rows.
 //   A operand = the batch the loader would produce: fp32 records cast with cvt.rn to bf16 / f16,
 //   16-bit records copied; W (and the MMA's input kind) in that same 16-bit type.
 //   Rows resolve through the shard views (owner v mod W, HBM / pinned spill / peer HBM), so spilled
@@ -645,8 +647,9 @@ cudaError_t launch_gather_linear(const LinearArgs& a_in, bool pdl, cudaStream_t 
 namespace {
 constexpr int kKcChunk = 64;                     // K elements per chunk (one 128-B swizzle row of bf16)
 // Shared memory at D = 512 (224 KB): 2 W stages of a whole 64-row chunk (128 KB) + 4 slots of 16 KB
-// (A stages; with fp32 records gathered by TMA, 2 A stages + 2 fp32 staging halves) + the epilogue
-// staging (32 KB).  Experiment layout (debug bit 2048): 3 half-chunk W stages (96 KB) + 6 slots.
+// (A stages; with fp32 records gathered by TMA, 2 slot pairs: fp32 halves converted in place) + the
+// epilogue staging (32 KB).  Experiment layout (debug bit 2048): 3 half-chunk W stages (96 KB) +
+// 6 slots.  CTA pairs (kPair): 4 W stages of half a chunk's columns (32 KB each).
 constexpr int kKcASlots = 6;   // max 16 KB A / staging slots
 constexpr int kKcWStages = 4;  // max W stages of one 32-row half chunk (D / 64 boxes of 32 x 64)
 constexpr int kKcABytes = kTileM * 128;          // 16 KB: 128 rows x 64 bf16
@@ -1241,7 +1244,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     else
       run(std::integral_constant<int, 4>{});
   } else if (warp == kKcLoaderWarp) {
-    // ---------------- W loader: the same (tile, chunk) sequence; chunk ch of W_k into stage u % 2
+    // ---------------- W loader: the same (tile, chunk) sequence; chunk ch of W_k into the next stage
+    // of the ring (or, W_k resident, chunk ch into stage ch once)
     if (lane == 0) {
       const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
       const uint32_t nbox = static_cast<uint32_t>(D / npeer / 64);
