@@ -15,6 +15,16 @@ ge.build()
 import paper_2504_13266_b200 as pp  # noqa: E402
 
 n, m, F, K = 2_449_029, 61_859_140, 100, 3
+L2FETCH = None
+if os.environ.get("PROP_L2FETCH"):  # experiment: the context's max L2 fetch granularity (bytes)
+    import ctypes
+    torch.zeros(1, device="cuda")
+    cu = ctypes.CDLL("libcuda.so.1")
+    val = ctypes.c_size_t(int(os.environ["PROP_L2FETCH"]))
+    rc = cu.cuCtxSetLimit(ctypes.c_int(5), val)  # CU_LIMIT_MAX_L2_FETCH_GRANULARITY
+    got = ctypes.c_size_t(0)
+    cu.cuCtxGetLimit(ctypes.byref(got), ctypes.c_int(5))
+    L2FETCH = {"set": int(os.environ["PROP_L2FETCH"]), "rc": rc, "got": got.value}
 g = torch.Generator(device="cuda").manual_seed(2504)
 src = torch.randint(0, n, (m,), device="cuda", generator=g)
 dst = torch.randint(0, n, (m,), device="cuda", generator=g)
@@ -67,7 +77,8 @@ print(json.dumps({"config": "products-sized ER graph", "n": n, "nnz": nnz, "F": 
                   "ms_per_hop": ms / K, "compulsory_bytes_per_hop": compulsory,
                   "compulsory_GBs": compulsory * K / ms / 1e6, "gather_bytes_per_hop": gather_bytes,
                   "gather_GBs": gather_bytes * K / ms / 1e6,
-                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (row kernels; PPLOAD_SPMM=sliced opt-in)")}))
+                  "kernel": os.environ.get("PPLOAD_SPMM", "auto (row kernels; PPLOAD_SPMM=sliced opt-in)"),
+                  "l2_fetch": L2FETCH}))
 
 # Same graph, propagated INTO a loader store (pp_propagate_store: node-major [n, K+1, F] fp32
 # records, hop slot k from slot k-1, weights from the degree array on the fly).
@@ -96,5 +107,5 @@ print(json.dumps({"config": "products-sized ER graph, into the loader store",
                   "kernel": os.environ.get("PPLOAD_SPMM", "auto (row kernels; PPLOAD_SPMM=sliced opt-in)"), "n": n,
                   "nnz": nnz, "F": F, "K": K, "ms": ms, "algorithmic_GBs": K * per_hop / ms / 1e6,
                   "compulsory_GBs": compulsory * K / ms / 1e6, "gather_GBs": gather_bytes * K / ms / 1e6,
-                  "frac_hbm": K * per_hop / ms / 1e6 / peak, "ms_per_hop": ms / K}))
+                  "frac_hbm": K * per_hop / ms / 1e6 / peak, "ms_per_hop": ms / K, "l2_fetch": L2FETCH}))
 L.close()
