@@ -169,6 +169,32 @@ cudaError_t launch_spmm_sliced_rows(int64_t n, int32_t F, const int64_t* row_ptr
 // Into a W = 1 loader store (slot a.k from slot a.k - 1; a.col32 required).
 cudaError_t launch_spmm_store_sliced(const StorePropArgs& a, uint8_t* scratch, int64_t nnz, cudaStream_t st);
 int64_t spmm_sliced_scratch_bytes(int64_t rows, int32_t F, int64_t nnz);
+// Wave-synchronous propagation (propagate.cu, k_spmm_wave): W = 1, F % 4 == 0, F <= 128, every
+// row in HBM.  y row i (dst + i * dst_stride, fp32) = sum over the CSR row of w_ij * x row j
+// (src + j * src_stride); weights val[p] or, with val == null, 1/sqrt(d~_i deg[j]).
+struct WaveArgs {
+  int64_t n = 0, ncols = 0;  // output rows; column-id range (windows split [0, ncols))
+  int32_t F = 0, nv = 0;     // nv = F / 4 (set by the launcher)
+  const int64_t* row_ptr = nullptr;
+  const int64_t* col = nullptr;
+  const double* val = nullptr;
+  const int32_t* deg = nullptr;
+  const uint8_t* src = nullptr;
+  int64_t src_stride = 0;    // bytes
+  uint8_t* dst = nullptr;
+  int64_t dst_stride = 0;
+  uint8_t* xdst = nullptr;   // optional 16-bit copy of the output rows (exchange copy slot)
+  int64_t x_stride = 0;
+  int32_t x_dtype = 1;       // 1 bf16, 2 f16
+  // set by launch_spmm_wave
+  int32_t R = 0, C = 0, lag = 0, spin = 0;
+  int64_t win = 0;
+  unsigned* sync = nullptr;
+};
+bool spmm_wave_eligible(int32_t F, const void* src, int64_t src_stride, const void* dst, int64_t dst_stride);
+bool spmm_use_wave(int64_t n, int32_t F);
+// sync: 4 bytes of device scratch (zeroed here, stream-ordered).
+cudaError_t launch_spmm_wave(WaveArgs a, unsigned* sync, cudaStream_t st);
 bool spmm_use_sliced(int64_t rows, int32_t F);
 
 // ---- DMA-staged assembly (gather.cu): out row j = cast(stage record j) ----------

@@ -171,6 +171,7 @@ struct pp_loader {
   uint32_t* d_col32 = nullptr;  // int32 column ids for the L2-sliced propagation (pp_propagate_store)
   int64_t col32_cap = 0;
   uint8_t* d_xt = nullptr;      // its window-major copy of the input hop slot
+  void* d_wave_sync = nullptr;  // window counter of the wave-synchronous propagation
   int64_t xt_cap = 0;
   int64_t scratch_bytes = 0;  // HBM of order / sort / exchange buffers allocated so far
 
@@ -231,6 +232,7 @@ void release(pp_loader* L) {
   cudaFree(L->d_flags);
   cudaFree(L->d_col32);
   cudaFree(L->d_xt);
+  cudaFree(L->d_wave_sync);
   if (L->cstream) cudaStreamDestroy(L->cstream);
   if (!L->borrowed) cudaFree(L->d_store);
   cudaFree(L->d_xstore);
@@ -532,10 +534,31 @@ pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64
   if (cudaMallocFromPoolAsync(reinterpret_cast<void**>(&val), static_cast<size_t>(nnz) * sizeof(double), pools[dev],
                               st) != cudaSuccess)
     return fail(PP_ERR_OOM, "operator values (%lld nonzeros)", (long long)nnz);
+  // wave-synchronous kernel (propagate.cu) for large graphs: the same arithmetic, a fraction of
+  // the DRAM traffic; it needs a 4-byte window counter
+  unsigned* wave_sync = nullptr;
+  const bool wave = spmm_use_wave(n, F) && spmm_wave_eligible(F, X, int64_t(F) * 4, hops, int64_t(F) * 4) &&
+                    cudaMallocFromPoolAsync(reinterpret_cast<void**>(&wave_sync), 256, pools[dev], st) == cudaSuccess;
   e = launch_operator_values(n, row_ptr, col_idx, val, st);
-  for (int32_t k = 1; k <= K && e == cudaSuccess; ++k)
-    e = launch_spmm(n, F, row_ptr, col_idx, val, hops + (k - 1) * (plane / sizeof(float)),
-                    hops + k * (plane / sizeof(float)), st);
+  for (int32_t k = 1; k <= K && e == cudaSuccess; ++k) {
+    const float* x = hops + (k - 1) * (plane / sizeof(float));
+    float* y = hops + k * (plane / sizeof(float));
+    if (wave) {
+      WaveArgs a;
+      a.n = a.ncols = n;
+      a.F = F;
+      a.row_ptr = row_ptr;
+      a.col = col_idx;
+      a.val = val;
+      a.src = reinterpret_cast<const uint8_t*>(x);
+      a.dst = reinterpret_cast<uint8_t*>(y);
+      a.src_stride = a.dst_stride = int64_t(F) * 4;
+      e = launch_spmm_wave(a, wave_sync, st);
+    } else {
+      e = launch_spmm(n, F, row_ptr, col_idx, val, x, y, st);
+    }
+  }
+  if (wave_sync) cudaFreeAsync(wave_sync, st);
   cudaFreeAsync(val, st);
   if (e != cudaSuccess) return fail(PP_ERR_CUDA, "propagation: %s", cudaGetErrorString(e));
   return PP_OK;
@@ -821,7 +844,35 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
       nnz_sliced = nnz;
     }
   }
-  PPL_CUDA(L, sliced ? launch_spmm_store_sliced(a, L->d_xt, nnz_sliced, user) : launch_spmm_store(a, user));
+  const ShardView& me = L->shards[L->rank];
+  if (!sliced && L->W == 1 && me.n_hbm == L->local_rows && spmm_use_wave(L->local_rows, L->F) &&
+      spmm_wave_eligible(L->F, me.hbm, L->rec_stride, me.hbm, L->rec_stride)) {
+    // wave-synchronous kernel (propagate.cu): slot k of every record from slot k - 1
+    if (!L->d_wave_sync) {
+      if (cudaMalloc(&L->d_wave_sync, 256) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PP_ERR_OOM, "propagation counter (256 B)");
+      }
+      L->scratch_bytes += 256;
+    }
+    WaveArgs w;
+    w.n = w.ncols = L->local_rows;
+    w.F = L->F;
+    w.row_ptr = row_ptr;
+    w.col = col_idx;
+    w.deg = deg;
+    w.src = me.hbm + static_cast<int64_t>(k - 1) * L->F * 4;
+    w.dst = const_cast<uint8_t*>(me.hbm) + static_cast<int64_t>(k) * L->F * 4;
+    w.src_stride = w.dst_stride = L->rec_stride;
+    if (L->d_xstore) {
+      w.xdst = L->d_xstore + static_cast<int64_t>(k) * L->F * 2;
+      w.x_stride = L->xrec_stride;
+      w.x_dtype = a.x_dtype;
+    }
+    PPL_CUDA(L, launch_spmm_wave(w, static_cast<unsigned*>(L->d_wave_sync), user));
+  } else {
+    PPL_CUDA(L, sliced ? launch_spmm_store_sliced(a, L->d_xt, nnz_sliced, user) : launch_spmm_store(a, user));
+  }
   if (user != L->stream) {  // ... and later loader work after this hop
     PPL_CUDA(L, cudaEventRecord(L->ev_out, user));
     PPL_CUDA(L, cudaStreamWaitEvent(L->stream, L->ev_out, 0));

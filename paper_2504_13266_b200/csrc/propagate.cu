@@ -605,6 +605,212 @@ cudaError_t launch_spmm_store(const StorePropArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---- wave-synchronous propagation (k_spmm_wave) ---------------------------------------------------
+// The row kernels above are bound by DRAM misses at products size: X_{k-1} (0.98 GB) is ~8x the L2,
+// every nonzero reads a random 400-B row, and 93 % of those rows miss (64.7 GB of DRAM reads per hop
+// for 50.5 GB of neighbour rows, profiles/r2/propagation_sliced.md).  Here the whole GPU works on one
+// *wave* of output rows at a time -- R rows per CTA, their fp64 partial sums resident in shared
+// memory -- and sweeps the column ids in C ascending windows of n / C ids, so at any moment all SMs
+// read neighbour rows from the same window of X_{k-1}: a row j that several rows of the wave need is
+// fetched from DRAM about once per wave instead of once per nonzero (S = grid * R rows per wave;
+// X row j has S d / n readers per wave).  Each output row's neighbours are still summed in ascending
+// column order (windows ascend; columns ascend inside a window) with the same separately rounded fp64
+// products and sums as k_spmm_rows_v4 / k_spmm_store_v4, and the weights are the same IEEE
+// expressions, so the result is bit-identical to them and to the oracle (O2/O3).
+// Work split: a warp takes 4 rows of its CTA; lanes 8q..8q+7 read the next 8 column ids of row q,
+// a ballot selects those inside the window, and the selected (row, column) entries are processed in
+// order, 4 neighbour rows in flight per warp, lane l owning features 4l..4l+3; a row saturating its 8
+// slots gets another round.  Between windows the CTAs keep loosely in step (a counter: before window
+// g a CTA waits, boundedly, until every CTA has finished window g - lag); the counter only shapes the
+// L2 working set -- no CTA reads another's results -- so the bounded wait cannot deadlock.
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wave_store16(uint8_t* p, int x_dtype, float4 y) {
+  store_x16(p, x_dtype, y.x, y.y);
+  store_x16(p + 4, x_dtype, y.z, y.w);
+}
+
+template <int kWaveThreads, int kWaveAhead>
+__global__ void __launch_bounds__(kWaveThreads, 1) k_spmm_wave(const WaveArgs a) {
+  constexpr int kWaveWarps = kWaveThreads / 32;
+  extern __shared__ __align__(16) uint8_t wsm[];
+  const int R = a.R, nv = a.nv;
+  double2* s_st = reinterpret_cast<double2*>(wsm);  // [R][2][nv]: features (4l, 4l+1), (4l+2, 4l+3) of lane l
+  int64_t* s_pos = reinterpret_cast<int64_t*>(s_st + static_cast<int64_t>(R) * 2 * nv);  // next nonzero
+  int64_t* s_end = s_pos + R;
+  double* s_di = reinterpret_cast<double*>(s_end + R);  // d~_i
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane >> 3, sl = lane & 7;
+  const bool on = lane < nv;
+  const int64_t S = static_cast<int64_t>(gridDim.x) * R;
+  const int64_t nwaves = (a.n + S - 1) / S;
+  for (int64_t wave = 0; wave < nwaves; ++wave) {
+    const int64_t row0 = wave * S + static_cast<int64_t>(blockIdx.x) * R;
+    const int rows = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(R), a.n - row0)));
+    for (int r = tid; r < rows; r += kWaveThreads) {
+      const int64_t b = a.row_ptr[row0 + r], e = a.row_ptr[row0 + r + 1];
+      s_pos[r] = b;
+      s_end[r] = e;
+      s_di[r] = static_cast<double>(e - b);
+    }
+    for (int i = tid; i < rows * 2 * nv; i += kWaveThreads) s_st[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int c = 0; c < a.C; ++c) {
+      const int64_t g = wave * a.C + c;
+      if (a.lag > 0 && g >= a.lag) {
+        if (tid == 0) {
+          const unsigned target = gridDim.x * static_cast<unsigned>(g - a.lag + 1);
+          for (int it = 0; it < a.spin && ld_relaxed_u32(a.sync) < target; ++it) __nanosleep(128);
+        }
+        __syncthreads();
+      }
+      const int64_t jend = c == a.C - 1 ? INT64_MAX : (c + 1) * a.win;
+      for (int r0 = warp * 4; r0 < rows; r0 += kWaveWarps * 4) {
+        unsigned active = 0xfu;
+        while (active) {
+          const int r = r0 + q;
+          const bool mine = r < rows && ((active >> q) & 1u);
+          int64_t j = 0;
+          double wl = 0.0;
+          bool in = false;
+          if (mine) {
+            const int64_t p = s_pos[r] + sl;
+            if (p < s_end[r]) {
+              j = a.col[p];
+              in = j < jend;
+              if (in)
+                wl = a.val != nullptr ? a.val[p]
+                                      : __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(s_di[r], static_cast<double>(a.deg[j]))));
+            }
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, in);  // also orders the s_pos reads before the update
+          unsigned sat = 0;  // rows whose 8 slots were all inside the window: they may have more
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sat |= (((mask >> (8 * t)) & 0xffu) == 0xffu ? 1u : 0u) << t;
+          if (sl == 0 && mine) s_pos[r] += __popc((mask >> (8 * q)) & 0xffu);
+          unsigned mm = mask;
+          int cur = -1;
+          double2 lo = make_double2(0.0, 0.0), hi = lo;
+          while (mm) {
+            float4 xv[kWaveAhead];
+            double w[kWaveAhead];
+            int rq[kWaveAhead];
+#pragma unroll
+            for (int u = 0; u < kWaveAhead; ++u) {
+              rq[u] = -1;
+              w[u] = 0.0;
+              xv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (mm) {  // warp-uniform
+                const int L = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const int64_t jj = __shfl_sync(0xffffffffu, j, L);
+                w[u] = __shfl_sync(0xffffffffu, wl, L);
+                rq[u] = L >> 3;
+                if (on) xv[u] = __ldcg(reinterpret_cast<const float4*>(a.src + jj * a.src_stride) + lane);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kWaveAhead; ++u) {
+              if (rq[u] < 0) break;
+              if (rq[u] != cur) {
+                double2* st = s_st + static_cast<int64_t>(r0 + rq[u]) * 2 * nv + lane;
+                if (cur >= 0 && on) {
+                  double2* so = s_st + static_cast<int64_t>(r0 + cur) * 2 * nv + lane;
+                  so[0] = lo;
+                  so[nv] = hi;
+                }
+                cur = rq[u];
+                if (on) {
+                  lo = st[0];
+                  hi = st[nv];
+                }
+              }
+              lo.x = __dadd_rn(lo.x, __dmul_rn(w[u], static_cast<double>(xv[u].x)));
+              lo.y = __dadd_rn(lo.y, __dmul_rn(w[u], static_cast<double>(xv[u].y)));
+              hi.x = __dadd_rn(hi.x, __dmul_rn(w[u], static_cast<double>(xv[u].z)));
+              hi.y = __dadd_rn(hi.y, __dmul_rn(w[u], static_cast<double>(xv[u].w)));
+            }
+          }
+          if (cur >= 0 && on) {
+            double2* so = s_st + static_cast<int64_t>(r0 + cur) * 2 * nv + lane;
+            so[0] = lo;
+            so[nv] = hi;
+          }
+          __syncwarp();
+          active = sat;
+        }
+      }
+      __syncthreads();
+      if (a.lag > 0 && tid == 0) atomicAdd(a.sync, 1u);
+    }
+    // the wave's rows are complete: one RNE rounding to fp32 (+ the optional 16-bit copy)
+    for (int r = warp; r < rows; r += kWaveWarps) {
+      if (on) {
+        const double2* st = s_st + static_cast<int64_t>(r) * 2 * nv + lane;
+        const double2 lo = st[0], hi = st[nv];
+        const float4 y = make_float4(__double2float_rn(lo.x), __double2float_rn(lo.y), __double2float_rn(hi.x),
+                                     __double2float_rn(hi.y));
+        reinterpret_cast<float4*>(a.dst + (row0 + r) * a.dst_stride)[lane] = y;
+        if (a.xdst != nullptr) wave_store16(a.xdst + (row0 + r) * a.x_stride + lane * 8, a.x_dtype, y);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+bool spmm_wave_eligible(int32_t F, const void* src, int64_t src_stride, const void* dst, int64_t dst_stride) {
+  return F % 4 == 0 && F <= 128 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(dst) % 16 == 0 && src_stride % 16 == 0 && dst_stride % 16 == 0;
+}
+
+// PPLOAD_SPMM=wave forces the wave kernel (when eligible), =rows|scalar|sliced the others; unset: wave
+// for graphs of at least PPLOAD_WAVE_MIN_ROWS rows (default 2^18).
+bool spmm_use_wave(int64_t n, int32_t F) {
+  const char* e = getenv("PPLOAD_SPMM");
+  if (e && *e) return !strcmp(e, "wave");
+  (void)F;
+  return n >= env_int("PPLOAD_WAVE_MIN_ROWS", 1 << 18);
+}
+
+size_t spmm_wave_smem(int32_t F, int32_t R) { return static_cast<size_t>(R) * (static_cast<size_t>(F) * 8 + 24); }
+
+cudaError_t launch_spmm_wave(WaveArgs a, unsigned* sync, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  int dev = 0, sms = 0, smem_max = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  a.nv = a.F / 4;
+  const int per_row = a.F * 8 + 24;
+  a.R = std::max(1, std::min(smem_max / per_row, env_int("PPLOAD_WAVE_ROWS", 1 << 30)));
+  const int64_t grid = std::min<int64_t>(sms, (a.n + a.R - 1) / a.R);
+  a.C = std::max(1, env_int("PPLOAD_WAVE_WINDOWS", 32));
+  a.lag = std::max(0, env_int("PPLOAD_WAVE_LAG", 2));
+  a.spin = env_int("PPLOAD_WAVE_SPIN", 20000);
+  a.win = (a.ncols + a.C - 1) / a.C;
+  a.sync = sync;
+  const size_t smem = spmm_wave_smem(a.F, a.R);
+  const int variant = env_int("PPLOAD_WAVE_VARIANT", 0);
+  void (*kern)(WaveArgs) = variant == 1 ? k_spmm_wave<1024, 4> : variant == 2 ? k_spmm_wave<512, 4> : k_spmm_wave<512, 8>;
+  const int threads = variant == 1 ? 1024 : 512;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess && a.lag > 0) e = cudaMemsetAsync(sync, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<uint32_t>(grid), threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_operator_values(int64_t n, const int64_t* row_ptr, const int64_t* col, double* val,
                                    cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
