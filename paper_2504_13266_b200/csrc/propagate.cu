@@ -773,13 +773,16 @@ bool spmm_wave_eligible(int32_t F, const void* src, int64_t src_stride, const vo
          reinterpret_cast<uintptr_t>(dst) % 16 == 0 && src_stride % 16 == 0 && dst_stride % 16 == 0;
 }
 
-// PPLOAD_SPMM=wave forces the wave kernel (when eligible), =rows|scalar|sliced the others; unset: wave
-// for graphs of at least PPLOAD_WAVE_MIN_ROWS rows (default 2^18).
+// Opt-in (PPLOAD_SPMM=wave): measured 3-4x slower than the row kernels at products size although it
+// cuts the DRAM reads by 30 % (r2 second session, profiles/r2/propagation_sliced.md): each warp's
+// (window, group) step is a chain of dependent round trips -- cursor, column ids, weights, neighbour
+// rows, partial sums -- for ~13 nonzeros, where the row kernel streams a row's nonzeros with its
+// column ids prefetched; the 30 % fewer bytes do not pay for the lost memory-level parallelism.
 bool spmm_use_wave(int64_t n, int32_t F) {
-  const char* e = getenv("PPLOAD_SPMM");
-  if (e && *e) return !strcmp(e, "wave");
+  (void)n;
   (void)F;
-  return n >= env_int("PPLOAD_WAVE_MIN_ROWS", 1 << 18);
+  const char* e = getenv("PPLOAD_SPMM");
+  return e && !strcmp(e, "wave");
 }
 
 size_t spmm_wave_smem(int32_t F, int32_t R) { return static_cast<size_t>(R) * (static_cast<size_t>(F) * 8 + 24); }

@@ -82,10 +82,10 @@ def test_hub_rows_saturate_their_slots(pp, monkeypatch, windows):
     assert np.array_equal(got.view(np.uint32), want_hops(rp, ci, X, K).view(np.uint32))
 
 
-def test_default_selection_at_scale(pp, monkeypatch):
-    # >= 2^18 rows take the wave kernel by default; the sqrt(d~) fixed point is independent of the
-    # oracle, and a sample of rows is compared with the oracle's per-row definition
-    monkeypatch.delenv("PPLOAD_SPMM", raising=False)
+def test_at_scale_fixed_point_and_sampled_rows(pp, monkeypatch):
+    # one full-size wave: the sqrt(d~) fixed point is independent of the oracle, and a sample of
+    # rows is compared with the per-row O3 definition written out
+    wave_env(monkeypatch, 1 << 20, 32)
     n, m = 300_000, 3_000_000
     rng = np.random.default_rng(4)
     rp, ci = oracle.build_csr(n, rng.integers(0, n, m), rng.integers(0, n, m))
