@@ -195,6 +195,10 @@ bool spmm_wave_eligible(int32_t F, const void* src, int64_t src_stride, const vo
 bool spmm_use_wave(int64_t n, int32_t F);
 // sync: 4 bytes of device scratch (zeroed here, stream-ordered).
 cudaError_t launch_spmm_wave(WaveArgs a, unsigned* sync, cudaStream_t st);
+// Row kernel with the neighbour rows staged in shared memory by cp.async (same WaveArgs; W = 1,
+// F % 4 == 0, F <= 128, every row in HBM); PPLOAD_SPMM=cp selects it.
+bool spmm_use_cp();
+cudaError_t launch_spmm_rows_cp(WaveArgs a, cudaStream_t st);
 bool spmm_use_sliced(int64_t rows, int32_t F);
 
 // ---- DMA-staged assembly (gather.cu): out row j = cast(stage record j) ----------

@@ -537,13 +537,15 @@ pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64
   // wave-synchronous kernel (propagate.cu) for large graphs: the same arithmetic, a fraction of
   // the DRAM traffic; it needs a 4-byte window counter
   unsigned* wave_sync = nullptr;
-  const bool wave = spmm_use_wave(n, F) && spmm_wave_eligible(F, X, int64_t(F) * 4, hops, int64_t(F) * 4) &&
+  const bool eligible = spmm_wave_eligible(F, X, int64_t(F) * 4, hops, int64_t(F) * 4);
+  const bool cp = eligible && spmm_use_cp();
+  const bool wave = !cp && eligible && spmm_use_wave(n, F) &&
                     cudaMallocFromPoolAsync(reinterpret_cast<void**>(&wave_sync), 256, pools[dev], st) == cudaSuccess;
   e = launch_operator_values(n, row_ptr, col_idx, val, st);
   for (int32_t k = 1; k <= K && e == cudaSuccess; ++k) {
     const float* x = hops + (k - 1) * (plane / sizeof(float));
     float* y = hops + k * (plane / sizeof(float));
-    if (wave) {
+    if (wave || cp) {
       WaveArgs a;
       a.n = a.ncols = n;
       a.F = F;
@@ -553,7 +555,7 @@ pp_status pp_propagate(int64_t n, int32_t F, const int64_t* row_ptr, const int64
       a.src = reinterpret_cast<const uint8_t*>(x);
       a.dst = reinterpret_cast<uint8_t*>(y);
       a.src_stride = a.dst_stride = int64_t(F) * 4;
-      e = launch_spmm_wave(a, wave_sync, st);
+      e = cp ? launch_spmm_rows_cp(a, st) : launch_spmm_wave(a, wave_sync, st);
     } else {
       e = launch_spmm(n, F, row_ptr, col_idx, val, x, y, st);
     }
@@ -845,10 +847,11 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
     }
   }
   const ShardView& me = L->shards[L->rank];
-  if (!sliced && L->W == 1 && me.n_hbm == L->local_rows && spmm_use_wave(L->local_rows, L->F) &&
+  const bool cp = spmm_use_cp();
+  if (!sliced && L->W == 1 && me.n_hbm == L->local_rows && (cp || spmm_use_wave(L->local_rows, L->F)) &&
       spmm_wave_eligible(L->F, me.hbm, L->rec_stride, me.hbm, L->rec_stride)) {
-    // wave-synchronous kernel (propagate.cu): slot k of every record from slot k - 1
-    if (!L->d_wave_sync) {
+    // wave-synchronous or cp.async-staged row kernel (propagate.cu): slot k of every record from slot k - 1
+    if (!cp && !L->d_wave_sync) {
       if (cudaMalloc(&L->d_wave_sync, 256) != cudaSuccess) {
         cudaGetLastError();
         return fail(PP_ERR_OOM, "propagation counter (256 B)");
@@ -869,7 +872,7 @@ pp_status pp_propagate_store(pp_loader* L, int32_t k, const int64_t* row_ptr, co
       w.x_stride = L->xrec_stride;
       w.x_dtype = a.x_dtype;
     }
-    PPL_CUDA(L, launch_spmm_wave(w, static_cast<unsigned*>(L->d_wave_sync), user));
+    PPL_CUDA(L, cp ? launch_spmm_rows_cp(w, user) : launch_spmm_wave(w, static_cast<unsigned*>(L->d_wave_sync), user));
   } else {
     PPL_CUDA(L, sliced ? launch_spmm_store_sliced(a, L->d_xt, nnz_sliced, user) : launch_spmm_store(a, user));
   }

@@ -768,6 +768,170 @@ static int env_int(const char* name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
+// ---- row kernel with the neighbour rows staged by cp.async (k_spmm_rows_cp) -------------------------
+// k_spmm_rows_v4 / k_spmm_store_v4 keep 4 neighbour rows in flight per warp in registers (32 warps
+// per SM: ~51 KB), and at products size they are bound by that memory-level parallelism against
+// random 400-B rows that miss L2 93 % of the time (5.4 TB/s of DRAM reads).  Here each warp streams
+// the nonzeros of its rows through a private ring of kSlots row buffers in shared memory, filled by
+// cp.async (LDGSTS, 16 B per lane, no register destination), so kSlots rows per warp -- 512 per SM
+// at 32 warps x 16 slots -- are in flight.  The ring runs across row boundaries: the nonzeros of a
+// warp's rows form one stream, issued kSlots ahead of the one being summed.  Lane l copies and later
+// reads only its own 16 bytes of each slot, so cp.async.wait_group orders everything (no barrier).
+// Summation per output row: ascending column order, separately rounded fp64 products and sums -- the
+// same arithmetic as the other row kernels, bit-identical to them and to the oracle (O2/O3).
+struct CpCursor {  // a position in the warp's stream of nonzeros
+  int64_t i, p, e;  // row, next nonzero, row end
+};
+
+template <int kThreads, int kSlots>
+__global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) {
+  extern __shared__ __align__(16) uint8_t csm[];
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = a.nv;
+  const bool on = lane < nv;
+  const int64_t row_bytes = static_cast<int64_t>(nv) * 16;
+  uint8_t* ring = csm + static_cast<int64_t>(warp) * kSlots * row_bytes + lane * 16;
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  if (first >= a.n) return;
+  // issue cursor: 32 column ids at a time, lane-parallel
+  CpCursor is{first, a.row_ptr[first], a.row_ptr[first + 1]};
+  int64_t ichunk = is.p;
+  int64_t jl = is.p + lane < is.e ? a.col[is.p + lane] : 0;
+  // consume cursor: 32 (column, weight) pairs at a time
+  CpCursor cs{first, 0, 0};
+  double di = 0.0;
+  int64_t cchunk = 0;
+  double wl = 0.0;
+  auto load_weights = [&]() {
+    const int64_t p = cchunk + lane;
+    wl = 0.0;
+    if (p < cs.e) {
+      if (a.val != nullptr) {
+        wl = a.val[p];
+      } else {
+        const int64_t j = a.col[p];
+        wl = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(di, static_cast<double>(a.deg[j]))));
+      }
+    }
+  };
+  auto put_row = [&](int64_t i, double2 lo, double2 hi) {  // one RNE rounding to fp32 (+ the 16-bit copy)
+    if (on) {
+      const float4 y = make_float4(__double2float_rn(lo.x), __double2float_rn(lo.y), __double2float_rn(hi.x),
+                                   __double2float_rn(hi.y));
+      reinterpret_cast<float4*>(a.dst + i * a.dst_stride)[lane] = y;
+      if (a.xdst != nullptr) wave_store16(a.xdst + i * a.x_stride + lane * 8, a.x_dtype, y);
+    }
+  };
+  // move the consume cursor onto the next row that has nonzeros (rows without any get zeros)
+  auto seek_row = [&]() -> bool {
+    for (; cs.i < a.n; cs.i += wstride) {
+      cs.p = a.row_ptr[cs.i];
+      cs.e = a.row_ptr[cs.i + 1];
+      if (cs.p < cs.e) {
+        di = static_cast<double>(cs.e - cs.p);
+        cchunk = cs.p;
+        load_weights();
+        return true;
+      }
+      put_row(cs.i, make_double2(0.0, 0.0), make_double2(0.0, 0.0));
+    }
+    return false;
+  };
+  // advance the issue cursor to the next nonzero of the stream (next row when this one is done)
+  auto issue = [&](int slot) {
+    while (is.p >= is.e && is.i < a.n) {  // empty rows are skipped (every row has its diagonal, but be safe)
+      is.i += wstride;
+      if (is.i >= a.n) break;
+      is.p = a.row_ptr[is.i];
+      is.e = a.row_ptr[is.i + 1];
+      ichunk = is.p;
+      jl = is.p + lane < is.e ? a.col[is.p + lane] : 0;
+    }
+    if (is.i < a.n) {
+      if (is.p - ichunk == 32) {
+        ichunk = is.p;
+        jl = is.p + lane < is.e ? a.col[is.p + lane] : 0;
+      }
+      const int64_t j = __shfl_sync(0xffffffffu, jl, static_cast<int>(is.p - ichunk));
+      if (on) {
+        const uint8_t* src = a.src + j * a.src_stride + lane * 16;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + slot * static_cast<uint32_t>(row_bytes)),
+                     "l"(src)
+                     : "memory");
+      }
+      ++is.p;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // possibly empty: keeps one group per stream slot
+  };
+#pragma unroll 1
+  for (int s = 0; s < kSlots; ++s) issue(s);
+  double2 lo = make_double2(0.0, 0.0), hi = lo;
+  int slot = 0;
+  bool more = seek_row();
+  while (more) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 1) : "memory");  // the oldest slot has landed
+    if (cs.p - cchunk == 32) {
+      cchunk = cs.p;
+      load_weights();
+    }
+    const double w = __shfl_sync(0xffffffffu, wl, static_cast<int>(cs.p - cchunk));
+    if (on) {
+      const float4 x = *reinterpret_cast<const float4*>(ring + slot * row_bytes);
+      lo.x = __dadd_rn(lo.x, __dmul_rn(w, static_cast<double>(x.x)));
+      lo.y = __dadd_rn(lo.y, __dmul_rn(w, static_cast<double>(x.y)));
+      hi.x = __dadd_rn(hi.x, __dmul_rn(w, static_cast<double>(x.z)));
+      hi.y = __dadd_rn(hi.y, __dmul_rn(w, static_cast<double>(x.w)));
+    }
+    __syncwarp();
+    issue(slot);  // refill the slot just summed (its smem read is complete: the sums above used it)
+    slot = slot + 1 == kSlots ? 0 : slot + 1;
+    if (++cs.p == cs.e) {
+      put_row(cs.i, lo, hi);
+      lo = make_double2(0.0, 0.0);
+      hi = lo;
+      cs.i += wstride;
+      more = seek_row();
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// PPLOAD_SPMM=cp forces it, =rows the register-staged row kernels.
+bool spmm_use_cp() {
+  const char* e = getenv("PPLOAD_SPMM");
+  return e && !strcmp(e, "cp");
+}
+
+cudaError_t launch_spmm_rows_cp(WaveArgs a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  int dev = 0, sms = 0, smem_max = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  a.nv = a.F / 4;
+  const int row_bytes = a.nv * 16;
+  const int variant = env_int("PPLOAD_CP_VARIANT", 0);
+  struct V {
+    void (*k)(WaveArgs);
+    int threads, slots;
+  };
+  const V vs[] = {{k_spmm_rows_cp<1024, 16>, 1024, 16}, {k_spmm_rows_cp<1024, 8>, 1024, 8},
+                  {k_spmm_rows_cp<512, 32>, 512, 32}, {k_spmm_rows_cp<1024, 12>, 1024, 12}};
+  V v = vs[variant >= 0 && variant < 4 ? variant : 0];
+  if (static_cast<int64_t>(v.threads / 32) * v.slots * row_bytes > smem_max) v = vs[3];
+  if (static_cast<int64_t>(v.threads / 32) * v.slots * row_bytes > smem_max) v = vs[1];
+  const size_t smem = static_cast<size_t>(v.threads / 32) * v.slots * row_bytes;
+  const int64_t grid = std::min<int64_t>(sms, (a.n + v.threads / 32 - 1) / (v.threads / 32));
+  e = cudaFuncSetAttribute(v.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  v.k<<<static_cast<uint32_t>(grid), v.threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 bool spmm_wave_eligible(int32_t F, const void* src, int64_t src_stride, const void* dst, int64_t dst_stride) {
   return F % 4 == 0 && F <= 128 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
          reinterpret_cast<uintptr_t>(dst) % 16 == 0 && src_stride % 16 == 0 && dst_stride % 16 == 0;

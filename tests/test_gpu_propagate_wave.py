@@ -128,3 +128,66 @@ def test_wave_and_row_kernels_agree_on_products_degree_mix(pp, monkeypatch):
     wave_env(monkeypatch, 1 << 20, 32)
     got = gpu_propagate(pp, rp, ci, X, 2)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+# ---- k_spmm_rows_cp: the row kernel with neighbour rows staged in shared memory by cp.async ----------
+def cp_env(monkeypatch, variant=0):
+    monkeypatch.setenv("PPLOAD_SPMM", "cp")
+    monkeypatch.setenv("PPLOAD_CP_VARIANT", str(variant))
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("n,m,F,K", [(1, 0, 4, 2), (300, 1500, 8, 3), (2000, 12000, 100, 2), (777, 9000, 128, 1),
+                                     (5000, 150000, 64, 2)])
+def test_cp_hop_major_bit_exact(pp, monkeypatch, variant, n, m, F, K):
+    # 1024 threads x 16 / 8 / 12 slots, 512 x 32: rings that wrap inside rows and across row boundaries
+    cp_env(monkeypatch, variant)
+    rp, ci = random_graph(n, m, n + m + F)
+    X = np.random.default_rng(F).standard_normal((n, F)).astype(np.float32)
+    got = gpu_propagate(pp, rp, ci, X, K)
+    assert np.array_equal(got.view(np.uint32), want_hops(rp, ci, X, K).view(np.uint32))
+
+
+def test_cp_hub_rows_and_empty_rows(pp, monkeypatch):
+    # a star (the hub row has n entries: its stream wraps the ring many times) plus rows with no
+    # nonzeros at all (a CSR the API accepts as long as nnz >= n): those rows must come out zero
+    n, F, K = 1500, 100, 2
+    leaves = np.setdiff1d(np.arange(1, n), [5, 6, 700])  # 5, 6, 700: only their diagonal, then none
+    rp, ci = oracle.build_csr(n, np.zeros(leaves.size, np.int64), leaves)
+    keep = np.ones(ci.shape[0], bool)
+    for i in (5, 6, 700):  # drop every entry of three leaf rows
+        keep[rp[i]:rp[i + 1]] = False
+    lens = np.diff(rp).copy()
+    lens[[5, 6, 700]] = 0
+    rp2 = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci2 = ci[keep]
+    X = np.random.default_rng(3).standard_normal((n, F)).astype(np.float32)
+    val = oracle.operator_values(n, rp2, ci2)
+    want = oracle.propagate(n, rp2, ci2, val, X, K)
+    cp_env(monkeypatch)
+    got = gpu_propagate(pp, rp2, ci2, X, K)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert not got[1][[5, 6, 700]].any()
+
+
+@pytest.mark.parametrize("n,m,F,K", [(1, 0, 4, 1), (1000, 9000, 100, 3), (700, 5000, 128, 2)])
+def test_cp_store_single_rank(pp, monkeypatch, n, m, F, K):
+    cp_env(monkeypatch)
+    rp, ci = random_graph(n, m, n + F)
+    X = np.random.default_rng(n).standard_normal((n, F)).astype(np.float32)
+    Ls = make_shards(pp, monkeypatch, 1, X, K + 1, batch_size=128, out_dtype=pp.PP_BF16)
+    propagate_all(Ls, rp, ci, K)
+    check_store(Ls, want_hops(rp, ci, X, K), K + 1, F)
+    for L in Ls:
+        L.close()
+
+
+def test_cp_and_row_kernels_agree_on_products_degree_mix(pp, monkeypatch):
+    n = 244_903
+    rp, ci = random_graph(n, n * 25, 7)
+    X = np.random.default_rng(8).standard_normal((n, 100)).astype(np.float32)
+    monkeypatch.setenv("PPLOAD_SPMM", "rows")
+    ref = gpu_propagate(pp, rp, ci, X, 2)
+    cp_env(monkeypatch)
+    got = gpu_propagate(pp, rp, ci, X, 2)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
