@@ -899,7 +899,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// PPLOAD_SPMM=cp forces it, =rows the register-staged row kernels.
+// Opt-in (PPLOAD_SPMM=cp): measured slower than k_spmm_rows_v4 / k_spmm_store_v4 (16.0 vs 12.1 ms per
+// products hop, profiles/r2/propagation_sliced.md): the per-lane 16-byte LDGSTS requests reach L2 as
+// 25 sector requests per 400-B row instead of a warp LDG.128's 13, for the same DRAM bytes.
 bool spmm_use_cp() {
   const char* e = getenv("PPLOAD_SPMM");
   return e && !strcmp(e, "cp");
