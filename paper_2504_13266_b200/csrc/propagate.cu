@@ -783,7 +783,9 @@ struct CpCursor {  // a position in the warp's stream of nonzeros
   int64_t i, p, e;  // row, next nonzero, row end
 };
 
-template <int kThreads, int kSlots>
+// kBulk: one cp.async.bulk per neighbour row (the whole 16-B-multiple row, issued by lane 0, completing
+// on a per-slot mbarrier) instead of 16 B per lane -- one request per row for the L2.
+template <int kThreads, int kSlots, bool kBulk>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) {
   extern __shared__ __align__(16) uint8_t csm[];
   constexpr int kWarps = kThreads / 32;
@@ -793,6 +795,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
   const int64_t row_bytes = static_cast<int64_t>(nv) * 16;
   uint8_t* ring = csm + static_cast<int64_t>(warp) * kSlots * row_bytes + lane * 16;
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const uint32_t ring0_s = ring_s - lane * 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(csm + static_cast<int64_t>(kWarps) * kSlots * row_bytes) + warp * kSlots;
+  const uint32_t bars_s = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  static_assert(kSlots <= 64, "one parity bit per slot");
+  uint64_t phase = 0;  // kBulk: parity bit per slot
+  if constexpr (kBulk) {
+    if (lane == 0)
+      for (int s = 0; s < kSlots; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars_s + 8 * s) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
   const int64_t first = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   if (first >= a.n) return;
@@ -856,7 +869,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
         jl = is.p + lane < is.e ? a.col[is.p + lane] : 0;
       }
       const int64_t j = __shfl_sync(0xffffffffu, jl, static_cast<int>(is.p - ichunk));
-      if (on) {
+      if constexpr (kBulk) {
+        if (lane == 0) {
+          const uint32_t bar = bars_s + 8 * slot;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's generic reads before the copy
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"(static_cast<uint32_t>(row_bytes))
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  ring0_s + slot * static_cast<uint32_t>(row_bytes)),
+              "l"(a.src + j * a.src_stride), "r"(static_cast<uint32_t>(row_bytes)), "r"(bar)
+              : "memory");
+        }
+      } else if (on) {
         const uint8_t* src = a.src + j * a.src_stride + lane * 16;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + slot * static_cast<uint32_t>(row_bytes)),
                      "l"(src)
@@ -864,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
       }
       ++is.p;
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");  // possibly empty: keeps one group per stream slot
+    if constexpr (!kBulk) asm volatile("cp.async.commit_group;" ::: "memory");  // possibly empty: one group per slot
   };
 #pragma unroll 1
   for (int s = 0; s < kSlots; ++s) issue(s);
@@ -872,7 +898,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
   int slot = 0;
   bool more = seek_row();
   while (more) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 1) : "memory");  // the oldest slot has landed
+    if constexpr (kBulk) {  // the oldest slot has landed
+      const uint32_t bar = bars_s + 8 * slot, par = static_cast<uint32_t>(phase >> slot) & 1u;
+      uint32_t done = 0;
+      do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(par)
+            : "memory");
+      } while (!done);
+      phase ^= 1ull << slot;
+    } else {
+      asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 1) : "memory");
+    }
     if (cs.p - cchunk == 32) {
       cchunk = cs.p;
       load_weights();
@@ -896,7 +935,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_rows_cp(const WaveArgs a) 
       more = seek_row();
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (!kBulk) asm volatile("cp.async.wait_all;" ::: "memory");
+  // kBulk: every issued copy was waited for (the issue cursor ends with the consume cursor)
 }
 
 // Opt-in (PPLOAD_SPMM=cp): measured slower than k_spmm_rows_v4 / k_spmm_store_v4 (16.0 vs 12.1 ms per
@@ -921,12 +961,15 @@ cudaError_t launch_spmm_rows_cp(WaveArgs a, cudaStream_t st) {
     void (*k)(WaveArgs);
     int threads, slots;
   };
-  const V vs[] = {{k_spmm_rows_cp<1024, 16>, 1024, 16}, {k_spmm_rows_cp<1024, 8>, 1024, 8},
-                  {k_spmm_rows_cp<512, 32>, 512, 32}, {k_spmm_rows_cp<1024, 12>, 1024, 12}};
-  V v = vs[variant >= 0 && variant < 4 ? variant : 0];
-  if (static_cast<int64_t>(v.threads / 32) * v.slots * row_bytes > smem_max) v = vs[3];
-  if (static_cast<int64_t>(v.threads / 32) * v.slots * row_bytes > smem_max) v = vs[1];
-  const size_t smem = static_cast<size_t>(v.threads / 32) * v.slots * row_bytes;
+  const V vs[] = {{k_spmm_rows_cp<1024, 16, false>, 1024, 16}, {k_spmm_rows_cp<1024, 8, false>, 1024, 8},
+                  {k_spmm_rows_cp<512, 32, false>, 512, 32},  {k_spmm_rows_cp<1024, 12, false>, 1024, 12},
+                  {k_spmm_rows_cp<1024, 12, true>, 1024, 12},  {k_spmm_rows_cp<1024, 8, true>, 1024, 8},
+                  {k_spmm_rows_cp<512, 24, true>, 512, 24},    {k_spmm_rows_cp<256, 48, true>, 256, 48}};
+  V v = vs[variant >= 0 && variant < 8 ? variant : 0];
+  auto bytes = [&](const V& x) { return static_cast<int64_t>(x.threads / 32) * x.slots * (row_bytes + 8); };
+  if (bytes(v) > smem_max) v = variant >= 4 ? vs[5] : vs[3];
+  if (bytes(v) > smem_max) v = vs[1];
+  const size_t smem = static_cast<size_t>(bytes(v));
   const int64_t grid = std::min<int64_t>(sms, (a.n + v.threads / 32 - 1) / (v.threads / 32));
   e = cudaFuncSetAttribute(v.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -136,11 +136,12 @@ def cp_env(monkeypatch, variant=0):
     monkeypatch.setenv("PPLOAD_CP_VARIANT", str(variant))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("n,m,F,K", [(1, 0, 4, 2), (300, 1500, 8, 3), (2000, 12000, 100, 2), (777, 9000, 128, 1),
                                      (5000, 150000, 64, 2)])
 def test_cp_hop_major_bit_exact(pp, monkeypatch, variant, n, m, F, K):
-    # 1024 threads x 16 / 8 / 12 slots, 512 x 32: rings that wrap inside rows and across row boundaries
+    # cp.async 16 B per lane: 1024 threads x 16 / 8 / 12 slots, 512 x 32; one cp.async.bulk per row:
+    # 1024 x 12 / 8, 512 x 24, 256 x 48 -- rings that wrap inside rows and across row boundaries
     cp_env(monkeypatch, variant)
     rp, ci = random_graph(n, m, n + m + F)
     X = np.random.default_rng(F).standard_normal((n, F)).astype(np.float32)
@@ -148,7 +149,8 @@ def test_cp_hop_major_bit_exact(pp, monkeypatch, variant, n, m, F, K):
     assert np.array_equal(got.view(np.uint32), want_hops(rp, ci, X, K).view(np.uint32))
 
 
-def test_cp_hub_rows_and_empty_rows(pp, monkeypatch):
+@pytest.mark.parametrize("variant", [0, 4])
+def test_cp_hub_rows_and_empty_rows(pp, monkeypatch, variant):
     # a star (the hub row has n entries: its stream wraps the ring many times) plus rows with no
     # nonzeros at all (a CSR the API accepts as long as nnz >= n): those rows must come out zero
     n, F, K = 1500, 100, 2
@@ -164,15 +166,16 @@ def test_cp_hub_rows_and_empty_rows(pp, monkeypatch):
     X = np.random.default_rng(3).standard_normal((n, F)).astype(np.float32)
     val = oracle.operator_values(n, rp2, ci2)
     want = oracle.propagate(n, rp2, ci2, val, X, K)
-    cp_env(monkeypatch)
+    cp_env(monkeypatch, variant)
     got = gpu_propagate(pp, rp2, ci2, X, K)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     assert not got[1][[5, 6, 700]].any()
 
 
+@pytest.mark.parametrize("variant", [0, 4])
 @pytest.mark.parametrize("n,m,F,K", [(1, 0, 4, 1), (1000, 9000, 100, 3), (700, 5000, 128, 2)])
-def test_cp_store_single_rank(pp, monkeypatch, n, m, F, K):
-    cp_env(monkeypatch)
+def test_cp_store_single_rank(pp, monkeypatch, variant, n, m, F, K):
+    cp_env(monkeypatch, variant)
     rp, ci = random_graph(n, m, n + F)
     X = np.random.default_rng(n).standard_normal((n, F)).astype(np.float32)
     Ls = make_shards(pp, monkeypatch, 1, X, K + 1, batch_size=128, out_dtype=pp.PP_BF16)
@@ -188,6 +191,7 @@ def test_cp_and_row_kernels_agree_on_products_degree_mix(pp, monkeypatch):
     X = np.random.default_rng(8).standard_normal((n, 100)).astype(np.float32)
     monkeypatch.setenv("PPLOAD_SPMM", "rows")
     ref = gpu_propagate(pp, rp, ci, X, 2)
-    cp_env(monkeypatch)
-    got = gpu_propagate(pp, rp, ci, X, 2)
-    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    for variant in (0, 4):
+        cp_env(monkeypatch, variant)
+        got = gpu_propagate(pp, rp, ci, X, 2)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), variant
