@@ -528,7 +528,15 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       ++i;
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // Z writes done before exit
+    // the staging buffers have been read before the CTA releases its shared memory; the Z writes
+    // themselves may still drain after exit (grid completion covers them, as for CUTLASS's TMA-store
+    // epilogues), so the next launch's CTA gets the SM a write latency earlier
+    if (lane == 0) {
+      if (a.debug & 131072)  // experiment: wait for the Z writes themselves before exit
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1411,7 +1419,12 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         arrive_leader(&t_empty[h]);
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0) {  // as in k_gather_linear
+      if (a.debug & 131072)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
   }
   if constexpr (kPair) {
     // no CTA leaves while the leader's MMAs may still read the peer's shared memory or signal its barriers

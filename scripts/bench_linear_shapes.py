@@ -24,11 +24,13 @@ D = 512
 pk = json.load(open("MEASURED_PEAKS.json")) if os.path.exists("MEASURED_PEAKS.json") else {}
 PEAK_HBM = pk.get("hbm_gbs", 6650.0)
 PEAK_TF = pk.get("bf16_tflops", 1590.0)
-SHAPES = {"igb_large": dict(H=3, F=1024, B=4096, dtype=pp.PP_F32, out=pp.PP_BF16, s_in=4),
+SHAPES = {"products": dict(H=4, F=100, B=8192, dtype=pp.PP_F32, out=pp.PP_BF16, s_in=4, rows=2_449_029),
+          "igb_large": dict(H=3, F=1024, B=4096, dtype=pp.PP_F32, out=pp.PP_BF16, s_in=4),
           "mag240m": dict(H=4, F=768, B=8192, dtype=pp.PP_F16, out=pp.PP_F16, s_in=2)}
 for name in os.environ.get("LIN_SHAPES", "igb_large,mag240m").split(","):
     c = SHAPES[name]
     H, F, B = c["H"], c["F"], c["B"]
+    ROWS = c.get("rows", int(os.environ.get("LIN_ROWS", 4_000_000)))
     L = pp.Loader(num_nodes=ROWS, num_hops=H, feat_dim=F, dtype=c["dtype"], batch_size=B, out_dtype=c["out"])
     L.fill_synthetic(2504)
     st = torch.cuda.Stream()
