@@ -1,5 +1,5 @@
 #!/bin/bash
-# (1) propagation bulk-copy variants (rerun after the parity-mask fix); (2) fused linear: Z-write wait at exit, A/B
+# (1) propagation bulk-copy variant 7 (256 x 48 slots; rerun after the 64-bit parity-mask fix); (2) fused linear: Z-write wait at exit, A/B
 O=gpurun_out; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/s2f_build.txt 2>&1
 timeout 300 python -m pytest tests/test_gpu_propagate_wave.py -q -x -ra -k cp > $O/s2f_pytest.txt 2>&1; echo "pytest rc=$?" >> $O/s2f_pytest.txt
@@ -7,12 +7,7 @@ timeout 600 python -m pytest tests/test_gpu_linear.py tests/test_gpu_linear_kc.p
 rm -f $O/s2f_prop.jsonl
 run() { env "$@" timeout 240 python scripts/bench_propagate.py | sed "s/^/{\"env\": \"$*\", \"r\": /; s/$/}/" >> $O/s2f_prop.jsonl 2>> $O/s2f_prop.err; }
 if grep -q "pytest rc=0" $O/s2f_pytest.txt; then
-  run PPLOAD_SPMM=rows
-  for v in 4 5 6 7; do run PPLOAD_SPMM=cp PPLOAD_CP_VARIANT=$v; done
-  run PPLOAD_SPMM=rows
-  for v in rows cp; do
-    PPLOAD_CP_VARIANT=4 PPLOAD_SPMM=$v PROP_ONE_HOP=1 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum,lts__t_requests_srcunit_tex_op_read.sum,lts__throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:"k_spmm" -c 1 --csv python scripts/bench_propagate.py > $O/s2f_ncu_$v.csv 2>> $O/s2f_prop.err
-  done
+  run PPLOAD_SPMM=cp PPLOAD_CP_VARIANT=7
 fi
 LIN_AB=0,131072 LIN_SHAPES=products,mag240m,igb_large timeout 1200 python scripts/bench_linear_shapes.py > $O/s2f_linear_ab.jsonl 2> $O/s2f_linear.err
 echo done
