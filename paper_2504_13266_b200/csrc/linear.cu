@@ -528,15 +528,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       ++i;
     }
-    // the staging buffers have been read before the CTA releases its shared memory; the Z writes
-    // themselves may still drain after exit (grid completion covers them, as for CUTLASS's TMA-store
-    // epilogues), so the next launch's CTA gets the SM a write latency earlier
-    if (lane == 0) {
-      if (a.debug & 131072)  // experiment: wait for the Z writes themselves before exit
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      else
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
+    // Z writes done before exit.  (Waiting only for the staging reads, .read, and letting the writes
+    // drain after exit measured the same -- r2 second session, profiles/r2/s2f_linear_exit_wait_ab.jsonl.)
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -1419,12 +1413,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         arrive_leader(&t_empty[h]);
       }
     }
-    if (lane == 0) {  // as in k_gather_linear
-      if (a.debug & 131072)
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      else
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // as in k_gather_linear
   }
   if constexpr (kPair) {
     // no CTA leaves while the leader's MMAs may still read the peer's shared memory or signal its barriers
