@@ -27,4 +27,9 @@ LIN_K=8 LIN_ROUNDS=1 timeout 600 ncu --set full --clock-control none --import-so
 LIN_SHAPES=mag240m timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather_linear_kc -s 20 -c 1 -o $O/r2s2_prof_linear_kc python scripts/bench_linear_shapes.py > /dev/null 2>> $O/r2s2_ncu.err
 PROP_ONE_HOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm_store_v4 -c 1 -o $O/r2s2_prof_spmm_store python scripts/bench_propagate.py > /dev/null 2>> $O/r2s2_ncu.err
 timeout 120 ./scripts/micro/hbm_ceiling > $O/r2s2_hbm_ceiling.jsonl 2>&1
+S=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck; do
+  timeout 900 $S --tool $tool --error-exitcode 9 python -m pytest -q tests/test_gpu_propagate_wave.py \
+    -k "not products and not at_scale" > $O/r2s2_sanitize_prop_$tool.txt 2>&1; echo "$tool rc=$?" >> $O/r2s2_sanitize_prop_$tool.txt
+done
 echo done
