@@ -24,6 +24,7 @@ D = 512
 pk = json.load(open("MEASURED_PEAKS.json")) if os.path.exists("MEASURED_PEAKS.json") else {}
 PEAK_HBM = pk.get("hbm_gbs", 6650.0)
 PEAK_TF = pk.get("bf16_tflops", 1590.0)
+PEAK_TF_SUST = pk.get("bf16_tflops_sustained", PEAK_TF)  # back-to-back cuBLAS for seconds (power-capped clocks)
 SHAPES = {"products": dict(H=4, F=100, B=8192, dtype=pp.PP_F32, out=pp.PP_BF16, s_in=4, rows=2_449_029),
           "igb_large": dict(H=3, F=1024, B=4096, dtype=pp.PP_F32, out=pp.PP_BF16, s_in=4),
           "mag240m": dict(H=4, F=768, B=8192, dtype=pp.PP_F16, out=pp.PP_F16, s_in=2)}
@@ -104,6 +105,7 @@ for name in os.environ.get("LIN_SHAPES", "igb_large,mag240m").split(","):
                       "ms_per_epoch": ms, "nodes_per_s": ROWS / ms * 1e3, "hbm_bytes_per_node": per_node,
                       "achieved_GBs": ROWS * per_node / ms / 1e6, "frac_hbm": ROWS * per_node / ms / 1e6 / PEAK_HBM,
                       "tflops": ROWS * flops / ms / 1e9, "frac_tensor": ROWS * flops / ms / 1e9 / PEAK_TF,
+                      "frac_tensor_sustained": ROWS * flops / ms / 1e9 / PEAK_TF_SUST,
                       "w_l2_bytes_per_node": H * F * D * 2 / 128, "clocks": clocks}), flush=True)
     L.close()
     del Z
