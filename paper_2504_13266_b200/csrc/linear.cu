@@ -696,8 +696,11 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
 __device__ __forceinline__ void bar_arrive_remote(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
+// relaxed: the arrival only posts the byte count the TMA's complete_tx will retire (the data is
+// ordered by the async proxy), so no release fence -- with .release every A / W stage posted a
+// MEMBAR on the issuing lane's path (r2 second session, profiles/r2/kc_issue/s2h_*)
 __device__ __forceinline__ void bar_expect_tx_remote(uint32_t caddr, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(caddr), "r"(tx)
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(caddr), "r"(tx)
                : "memory");
 }
 __device__ __forceinline__ void bar_wait_cluster(uint64_t* b, uint32_t parity) {
@@ -942,7 +945,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         const int lo = g * D / kEpiGroups, hi = (g + 1) * D / kEpiGroups;
         if (lo < (h + 1) * kUmmaN && hi > h * kUmmaN) cnt += 128;
       }
-      bar_init(&t_empty[h], cnt > 0 ? cnt * npeer : 1);
+      // pair mode: one (remote, release) arrival per epilogue warp instead of per thread
+      bar_init(&t_empty[h], cnt > 0 ? (kPair ? cnt / 32 : cnt) * npeer : 1);
     }
     bar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1410,7 +1414,12 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           }
         }
         tc_fence_before();
-        arrive_leader(&t_empty[h]);
+        if constexpr (kPair) {  // every lane's tcgen05.ld has completed (wait::ld) before the warp's arrival
+          __syncwarp();
+          if (lane == 0) arrive_leader(&t_empty[h]);
+        } else {
+          arrive_leader(&t_empty[h]);
+        }
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // as in k_gather_linear
