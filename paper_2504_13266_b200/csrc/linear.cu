@@ -905,6 +905,17 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     else
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
   };
+  // A stage written by this thread's generic stores (converters, register producers), after its
+  // fence.proxy.async: single CTAs arrive per thread (a local arrival is cheap); pairs arrive once
+  // per warp on the leader's barrier, since every remote release arrival costs a MEMBAR
+  auto arrive_a = [&](uint64_t* b) {
+    if constexpr (kPair) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) bar_arrive_remote(leader_addr(b));
+    } else {
+      bar_arrive(b);
+    }
+  };
   auto tma_bar = [&](uint64_t* b) -> uint32_t { return kPair ? leader_addr(b) : smem_addr(b); };
   auto wait_leader = [&](uint64_t* b, uint32_t parity) {  // a barrier the peer CTA also signals
     if constexpr (kPair)
@@ -927,7 +938,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kKcASlots; ++s) {
       // arrivals: TMA gathers (16-bit) one arrive + the bytes; fp32 converters 128; register producers 256
-      bar_init(&a_full[s], (a.tma_a ? 1 : a.tma_f32 ? 128 : kProducerThreads) * npeer);
+      bar_init(&a_full[s], (a.tma_a ? 1 : (a.tma_f32 ? 128 : kProducerThreads) / (kPair ? 32 : 1)) * npeer);
       bar_init(&a_empty[s], 1);
     }
     for (int s = 0; s < kKcASlots; ++s) {
@@ -1104,7 +1115,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           if (hh == 1) bar_arrive(&stg_empty[sl]);  // slot 2p + 1 read out; slot 2p now holds A(u)
         }
         fence_async_smem();
-        arrive_leader(&a_full[p]);
+        arrive_a(&a_full[p]);
       }
     }
   } else if (a.tma_a && warp < kProducerWarps) {  // warps 4-7
@@ -1184,7 +1195,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         }
       }
       fence_async_smem();
-      arrive_leader(&a_full[s]);
+      arrive_a(&a_full[s]);
     };
     // Register-staged loads keep only two chunks (64 KB per SM) in flight, less than HBM latency
     // needs, so each lane also pulls its row's chunk pf chunks ahead into L2 with one bulk prefetch
