@@ -696,6 +696,14 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
 __device__ __forceinline__ void bar_arrive_remote(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
+// Accumulator-empty arrival on the leader's barrier: the TMEM reads it publishes are ordered by
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync (and the leader's fence::after_thread_sync), not
+// by memory semantics, so the default arrive (CUTLASS's remote ClusterBarrier arrive): .release.cluster
+// compiles to MEMBAR.ALL.GPU, which also waited for the epilogue lane's outstanding Z bulk stores
+// (r2 second session: 5.7 % of the pair kernel's samples at that MEMBAR)
+__device__ __forceinline__ void bar_arrive_remote_tmem(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
 // relaxed: the arrival only posts the byte count the TMA's complete_tx will retire (the data is
 // ordered by the async proxy), so no release fence -- with .release every A / W stage posted a
 // MEMBAR on the issuing lane's path (r2 second session, profiles/r2/kc_issue/s2h_*)
@@ -1427,7 +1435,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         tc_fence_before();
         if constexpr (kPair) {  // every lane's tcgen05.ld has completed (wait::ld) before the warp's arrival
           __syncwarp();
-          if (lane == 0) arrive_leader(&t_empty[h]);
+          if (lane == 0) bar_arrive_remote_tmem(leader_addr(&t_empty[h]));
         } else {
           arrive_leader(&t_empty[h]);
         }
