@@ -657,6 +657,7 @@ constexpr int kKcWStages = 4;  // max W stages of one 32-row half chunk (D / 64 
 constexpr int kKcABytes = kTileM * 128;          // 16 KB: 128 rows x 64 bf16
 constexpr int kKcWBox = (kKcChunk / 2) * 128;    // 4 KB: 32 K rows x 64 columns (one half chunk)
 constexpr int kKcLoaderWarp = 9;
+constexpr int kKcRelayWarp = 10;  // pair mode, fp32 TMA path: forwards converted chunks to the leader
 
 // MN-major SW128 B descriptor; lbo = bytes between 64-column blocks (the K rows of a stage x 128 B)
 __device__ __forceinline__ uint64_t kc_w_desc(const void* p, uint32_t lbo) {
@@ -891,7 +892,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint64_t* stg_full = t_empty + 2;                       // [kKcASlots] fp32 staging halves (tma_f32)
   uint64_t* stg_empty = stg_full + kKcASlots;             // [kKcASlots]
   uint64_t* fin = stg_empty + kKcASlots;                  // pair mode: the leader's MMAs all complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint64_t* a_conv = fin + 1;                             // [kKcASlots] pair mode, fp32 TMA path: converted
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_conv + kKcASlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, F = a.F;
@@ -946,8 +948,11 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kKcASlots; ++s) {
       // arrivals: TMA gathers (16-bit) one arrive + the bytes; fp32 converters 128; register producers 256
-      bar_init(&a_full[s], (a.tma_a ? 1 : (a.tma_f32 ? 128 : kProducerThreads) / (kPair ? 32 : 1)) * npeer);
+      // pair mode: converted chunks reach the leader through one relay arrival per CTA, register
+      // producers arrive once per warp
+      bar_init(&a_full[s], (a.tma_a ? 1 : a.tma_f32 ? (kPair ? 1 : 128) : kProducerThreads / (kPair ? 32 : 1)) * npeer);
       bar_init(&a_empty[s], 1);
+      bar_init(&a_conv[s], 128);
     }
     for (int s = 0; s < kKcASlots; ++s) {
       bar_init(&stg_full[s], 1);
@@ -1123,7 +1128,10 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           if (hh == 1) bar_arrive(&stg_empty[sl]);  // slot 2p + 1 read out; slot 2p now holds A(u)
         }
         fence_async_smem();
-        arrive_a(&a_full[p]);
+        if constexpr (kPair)
+          bar_arrive(&a_conv[p]);  // the relay warp forwards it to the leader
+        else
+          bar_arrive(&a_full[p]);
       }
     }
   } else if (a.tma_a && warp < kProducerWarps) {  // warps 4-7
@@ -1358,6 +1366,20 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
     }
     __syncwarp();
+  } else if (kPair && a.tma_f32 && warp == kKcRelayWarp) {
+    // ---------------- pair mode, fp32 records: one lane forwards "chunk u converted" (the 128 converter
+    // threads' local arrivals, acquired here) to the leader's a_full with one cluster-scope release per
+    // chunk -- a per-warp release.cluster arrival on the converters' own path (MEMBAR.ALL.GPU each) made
+    // the pair 1.3x slower than single CTAs at IGB-large rows (r2 second session)
+    if (lane == 0) {
+      Ring ra(na);
+      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q))
+        for (int ch = 0; ch < nch; ++ch, ra.next()) {
+          bar_wait(&a_conv[ra.s], ra.ph);
+          bar_arrive_remote(leader_addr(&a_full[ra.s]));
+        }
+    }
+    __syncwarp();
   } else if (warp >= kEpiWarp0) {
     // ---------------- epilogue (as in k_gather_linear)
     const int e = warp & 3;
@@ -1468,7 +1490,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
 static size_t linear_kc_smem_bytes(int D) {
   (void)D;  // the layout is sized for D = 512 (z_s at a fixed offset)
   return 1024 + static_cast<size_t>(kKcWStages) * (512 / 64) * kKcWBox + 4 * kKcABytes + 64 +
-         kEpiWarps * kEpiBufs * kStageBytes + 256;
+         kEpiWarps * kEpiBufs * kStageBytes + 512;
 }
 
 bool linear_kc_supported(int H, int F, int D, int num_sms, int in_dtype, int out_dtype) {
