@@ -652,7 +652,7 @@ constexpr int kKcChunk = 64;                     // K elements per chunk (one 12
 // (A stages; with fp32 records gathered by TMA, 2 slot pairs: fp32 halves converted in place) + the
 // epilogue staging (32 KB).  Experiment layout (debug bit 2048): 3 half-chunk W stages (96 KB) +
 // 6 slots.  CTA pairs (kPair): 4 W stages of half a chunk's columns (32 KB each).
-constexpr int kKcASlots = 6;   // max 16 KB A / staging slots
+constexpr int kKcASlots = 8;   // max 16 KB A / staging slots
 constexpr int kKcWStages = 4;  // max W stages of one 32-row half chunk (D / 64 boxes of 32 x 64)
 constexpr int kKcABytes = kTileM * 128;          // 16 KB: 128 rows x 64 bf16
 constexpr int kKcWBox = (kKcChunk / 2) * 128;    // 4 KB: 32 K rows x 64 columns (one half chunk)
@@ -877,8 +877,12 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   const int wrows = kKcChunk / wsplit;                    // K rows per W stage
   const int wbrows = six ? 32 : 64;                       // K rows per W TMA box (must match encode_w_map_kc)
   const int w_stage_bytes = (D / npeer / 64) * wrows * 128;
-  const int nws = six ? 3 : 2 * npeer;                    // W stages
-  const int nas = six ? 6 : 4;                            // A / staging slots
+  // Pairs: a W stage is half a chunk's columns (32 KB at D = 512), so 2 W stages leave room for 8 A
+  // slots (4 fp32 chunk pairs in flight); experiment bit 65536: the first pair layout, 4 W stages + 4
+  // slots (A ring 2 deep on the fp32 path: 1.3x slower than single CTAs at IGB-large rows)
+  const bool pair_old = kPair && (a.debug & 65536) != 0;
+  const int nws = six ? 3 : (pair_old ? 4 : 2);           // W stages
+  const int nas = six ? 6 : (kPair && !pair_old ? 8 : 4); // A / staging slots
   uint8_t* w_s = smem;                                    // [nws][D / 64 blocks][wrows K rows][128 B]
   uint8_t* a_s = w_s + nws * w_stage_bytes;               // [nas][128 rows][128 B]
   uint8_t* z_s = w_s + 4 * ((512 / 64) * kKcWBox) + 4 * kKcABytes;  // epilogue staging (fixed offset)
@@ -935,8 +939,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   };
   const int nh = D / kUmmaN;
   const int nch = (F + kKcChunk - 1) / kKcChunk;
-  // every W chunk of hop k fits the W stages (F <= 128; <= 256 for pairs): load W_k once and keep it
-  const bool wres = nch * (kKcChunk / (six ? 32 : 64)) <= (six ? 3 : 2 * npeer) && !six;
+  // every W chunk of hop k fits the W stages (F <= 128): load W_k once and keep it
+  const bool wres = nch * (kKcChunk / (six ? 32 : 64)) <= nws && !six;
   const int s_in = a.in_dtype == 0 ? 4 : 2;
   // A stages: one per slot (16-bit TMA gathers, register producers); fp32 TMA gathers use the slots in
   // pairs: chunk u's two 32-element fp32 halves (128 rows x 128 B, SW128) land in slots 2p and 2p + 1
