@@ -880,9 +880,10 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   // Pairs: a W stage is half a chunk's columns (32 KB at D = 512), so 2 W stages leave room for 8 A
   // slots (4 fp32 chunk pairs in flight); experiment bit 65536: the first pair layout, 4 W stages + 4
   // slots (A ring 2 deep on the fp32 path: 1.3x slower than single CTAs at IGB-large rows)
-  const bool pair_old = kPair && (a.debug & 65536) != 0;
-  const int nws = six ? 3 : (pair_old ? 4 : 2);           // W stages
-  const int nas = six ? 6 : (kPair && !pair_old ? 8 : 4); // A / staging slots
+  // experiment bit 131072: 3 W stages + 6 slots
+  const int pair_ws = !kPair ? 2 : (a.debug & 65536) ? 4 : (a.debug & 131072) ? 3 : 2;
+  const int nws = six ? 3 : pair_ws;                      // W stages
+  const int nas = six ? 6 : (kPair ? 12 - 2 * pair_ws : 4);  // A / staging slots (pairs: 192 KB in all)
   uint8_t* w_s = smem;                                    // [nws][D / 64 blocks][wrows K rows][128 B]
   uint8_t* a_s = w_s + nws * w_stage_bytes;               // [nas][128 rows][128 B]
   uint8_t* z_s = w_s + 4 * ((512 / 64) * kKcWBox) + 4 * kKcABytes;  // epilogue staging (fixed offset)
