@@ -1585,10 +1585,13 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
     a.tma_f32 = encode_a_map_f32_kc(a, &amap) ? 1 : 0;
-  // CTA pairs (cta_group::2, M = 256), opt-in with PPLOAD_LINEAR_PAIR=1: measured slower than
-  // single CTAs at every row shape (interleaved A/B, r2z*); experiment bit 8192 flips the choice
+  // CTA pairs (cta_group::2, M = 256): the default when the A chunks come by TMA (HBM-resident,
+  // unsharded stores) -- half the W bytes through each SM's shared memory; interleaved A/B at MAG240M
+  // rows 13.0-13.6 vs 16.4-17.9 ms (single CTAs also drop further under the power cap), IGB-large rows
+  // 18.5-18.8 vs 19.0 ms (r2 second session, profiles/r2/kc_issue/s2*_ab_pair.jsonl).
+  // PPLOAD_LINEAR_PAIR=0/1 forces the choice; experiment bit 8192 flips it
   const char* pe = getenv("PPLOAD_LINEAR_PAIR");
-  bool pair = pe && !strcmp(pe, "1");
+  bool pair = pe && *pe ? !strcmp(pe, "1") : (a.tma_a || a.tma_f32);
   if (a.debug & 8192) pair = !pair;
   pair = pair && (a.num_sms / 2) >= a.H && (a.debug & 2048) == 0;
   a.pair = pair ? 1 : 0;
