@@ -124,6 +124,7 @@ struct LinearArgs {
   int32_t tma_a = 0;                    // set by launch_gather_linear_kc: A chunks by TMA tile::gather4
   int32_t tma_f32 = 0;                  // set by launch_gather_linear_kc: fp32 records by gather4 into staging
   int32_t pair = 0;                     // set by launch_gather_linear_kc: CTA pairs (cta_group::2, M = 256)
+  int32_t units = 0;                    // set by launch_gather_linear_kc: (tile, hop) units over the whole grid
 };
 bool linear_supported(int H, int F, int D, int num_sms);
 // The K-chunked kernel: F % 8 == 0, D in {256, 512}, 16-bit batch dtype.

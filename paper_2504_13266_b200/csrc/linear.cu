@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   const int H = a.H, F = a.F;
   const uint32_t cr = kPair ? cluster_rank() : 0u;       // rank in the pair (0 = leader)
   const int pid = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-  const int k = pid % H;
+  int k = pid % H;  // hop of the current unit: fixed per CTA, or per (tile, hop) unit with a.units
   const int q = pid / H, Q = (kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x)) / H;
   constexpr int kTM = kTileM * npeer;                     // rows per tile (the pair's)
   // barrier signals that go to the leader in pair mode
@@ -1021,6 +1021,26 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     }
     return total;
   };
+  // Work units.  Default: CTA (pair) pid is pinned to hop pid % H and walks tiles q, q + Q, ... (W_k
+  // may stay resident).  a.units (W streamed per tile anyway, TMA A paths): units u = tile * H + hop
+  // dealt round-robin over every CTA (pair) of the grid, so the grid is not rounded down to a multiple
+  // of H and the last wave is shared by all hops.  Every role walks the same unit sequence.
+  const int64_t ustride = a.units ? (kPair ? static_cast<int64_t>(gridDim.x >> 1) : static_cast<int64_t>(gridDim.x)) : Q;
+  const int64_t nunits = a.units ? total * H : total;
+  const int64_t ufirst = a.units ? pid : q;
+  auto unit_tile = [&](int64_t u) -> int64_t { return a.units ? u / H : u; };
+  auto next_unit = [&](int64_t u) -> int64_t {
+    for (; u < nunits; u += ustride) {
+      int64_t st_, ps_;
+      int r_;
+      if (tile_rows(unit_tile(u), st_, r_, ps_) > 0) return u;
+    }
+    return nunits;
+  };
+  auto set_unit = [&](int64_t u) -> int64_t {  // this unit's tile; sets k
+    if (a.units) k = static_cast<int>(u % H);
+    return unit_tile(u);
+  };
 
   const int gw = a.tma_a >= 2 ? 8 : 4;  // warps issuing gather4 (tma_a = 2: all eight producer warps)
   if ((a.tma_a || a.tma_f32) && warp < gw) {
@@ -1033,7 +1053,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     __shared__ int32_t s_rows[kTileM];
     const uint64_t amap_addr = reinterpret_cast<uint64_t>(&amap);
     Ring ra(na);
-    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+    for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride)) {
+      const int64_t t = set_unit(u);
       int64_t step, pos;
       int r0;
       const int rows = tile_rows_cta(t, step, r0, pos);
@@ -1097,7 +1118,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     const int tid = threadIdx.x - 128;
     const uint32_t a_base = smem_addr(a_s);
     Ring ra(na);
-    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+    for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride)) {
       for (int ch = 0; ch < nch; ++ch, ra.next()) {
         const int p = ra.s;
         const uint32_t at = a_base + 2 * p * kKcABytes;
@@ -1288,7 +1309,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       const uint64_t wmap_addr = reinterpret_cast<uint64_t>(&wmap);
       const uint32_t nbox = static_cast<uint32_t>(D / npeer / 64);
       Ring rw(nws);  // W stage fills: (tile, chunk, part) in order
-      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q)) {
+      for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride)) {
+        set_unit(u);
         for (int ch = 0; ch < nch; ++ch) {
           for (int wh = 0; wh < wsplit; ++wh, rw.next()) {
             const int s = rw.s;
@@ -1323,7 +1345,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           kPair ? ((kc_idesc(a.out_dtype) & ~(0x1Fu << 24)) | (static_cast<uint32_t>(kTM >> 4) << 24)) : kc_idesc(a.out_dtype);
       Ring ra(na), rw(nws);
       int i = 0;
-      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
+      for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride), ++i) {
         for (int ch = 0; ch < nch; ++ch, ra.next()) {
           const int sa = ra.s;
           wait_leader(&a_full[sa], ra.ph);
@@ -1378,7 +1400,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // the pair 1.3x slower than single CTAs at IGB-large rows (r2 second session)
     if (lane == 0) {
       Ring ra(na);
-      for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q))
+      for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride))
         for (int ch = 0; ch < nch; ++ch, ra.next()) {
           bar_wait(&a_conv[ra.s], ra.ph);
           bar_arrive_remote(leader_addr(&a_full[ra.s]));
@@ -1393,7 +1415,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     const int cols_per_slice = 128 / a.z_elem;
     const uint64_t zmap_addr = reinterpret_cast<uint64_t>(&zmap);
     int i = 0, slice = 0;
-    for (int64_t t = next_tile(q); t < total; t = next_tile(t + Q), ++i) {
+    for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride), ++i) {
+      const int64_t t = set_unit(u);
       int64_t step, pos;
       int r0;
       const int rows = tile_rows_cta(t, step, r0, pos);
@@ -1595,7 +1618,11 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   if (a.debug & 8192) pair = !pair;
   pair = pair && (a.num_sms / 2) >= a.H && (a.debug & 2048) == 0;
   a.pair = pair ? 1 : 0;
-  const int per = a.H * (pair ? 2 : 1);
+  // (tile, hop) work units over the whole grid when W_k is streamed per tile (F > 128) and the A
+  // chunks come by TMA (the register producers keep hop-pinned CTAs); experiment bit 262144: off
+  const bool w_resident = (a.F + kKcChunk - 1) / kKcChunk <= 2;
+  a.units = (a.tma_a || a.tma_f32) && !w_resident && (a.debug & (2048 | 262144)) == 0 ? 1 : 0;
+  const int per = a.units ? (pair ? 2 : 1) : a.H * (pair ? 2 : 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.num_sms / per) * per);
   cfg.blockDim = dim3(kLinThreads);
