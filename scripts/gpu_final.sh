@@ -29,7 +29,7 @@ PROP_ONE_HOP=1 timeout 900 ncu --set full --clock-control none --import-source o
 timeout 120 ./scripts/micro/hbm_ceiling > $O/r2s2_hbm_ceiling.jsonl 2>&1
 S=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck; do
-  timeout 900 $S --tool $tool --error-exitcode 9 python -m pytest -q tests/test_gpu_propagate_wave.py \
+  timeout 900 $S --tool $tool --num-cuda-barriers 65536 --error-exitcode 9 python -m pytest -q tests/test_gpu_propagate_wave.py \
     -k "not products and not at_scale" > $O/r2s2_sanitize_prop_$tool.txt 2>&1; echo "$tool rc=$?" >> $O/r2s2_sanitize_prop_$tool.txt
 done
 echo done
