@@ -321,7 +321,11 @@ pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_str
  *   D: 256 or 512.  F % 4 == 0 for fp32 records, F % 8 == 0 for 16-bit ones;
  *      any placement (HBM, spilled, sharded W > 1, compact store).  fp32 ->
  *      bf16 HBM stores with F <= 128 and W == 1 take the W-resident kernel,
- *      everything else the K-chunked one (PPLOAD_LINEAR=kc forces it).
+ *      everything else the K-chunked one (PPLOAD_LINEAR=kc forces it), which
+ *      runs as CTA pairs (tcgen05 cta_group::2, clusters of two) when the A
+ *      chunks come by TMA (an unsharded, HBM-resident store; PPLOAD_LINEAR_PAIR
+ *      = 0 / 1 forces single CTAs / pairs).  Results are identical either way
+ *      up to fp32 accumulation order.
  *   Z: device [n][B][H][D] of z_dtype (PP_BF16: RNE from fp32, or PP_F32),
  *      slot pitch z_stride_bytes (>= B*H*D*elem when n > 1), 16-B aligned.
  * W is read by TMA at every launch (nothing is cached across calls), so it may
