@@ -1069,6 +1069,28 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       __syncwarp();
       for (int ch = 0; ch < nch; ++ch) {
+        if (a.tma_f32 == 2) {  // fp32 records, wide boxes: the whole 64-element chunk (4 rows x 256 B per
+          if (lane == 0) {     // gather4, unswizzled) into slots 2p, 2p + 1 as 128 rows of 256 B
+            const int p = ra.s;
+            bar_wait(&a_empty[p], ra.ph ^ 1u);
+            bar_wait(&stg_empty[2 * p + 1], ra.ph ^ 1u);
+            ra.next();
+            if (warp == 0)
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[2 * p])),
+                           "r"(2 * kKcABytes)
+                           : "memory");
+            const int col = k * F + ch * kKcChunk;
+            uint8_t* dst = a_s + 2 * p * kKcABytes;
+            for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 1024)),
+                  "l"(amap_addr), "r"(col), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
+                  "r"(s_rows[4 * g + 3]), "r"(smem_addr(&stg_full[2 * p]))
+                  : "memory");
+          }
+          continue;
+        }
         if (a.tma_f32) {  // fp32 records: two 32-element halves into slots 2p, 2p + 1, converted by warps 4-7
           if (lane == 0) {
             const int p = ra.s;
@@ -1122,6 +1144,49 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int ch = 0; ch < nch; ++ch, ra.next()) {
         const int p = ra.s;
         const uint32_t at = a_base + 2 * p * kKcABytes;
+        if (a.tma_f32 == 2) {
+          // wide boxes: staging row r = 256 B (64 fp32) at 2p * 16 KB + 256 r; the A chunk (rows of 128 B,
+          // SW128) overwrites staging rows 0-63, which other warps' threads read -- so every thread reads
+          // all of its items first, the four converter warps meet at a named barrier, then write
+          bar_wait(&stg_full[2 * p], ra.ph);
+          uint4 x[4][2][2];
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int item = tid + 128 * it;
+            const int r = item >> 2, j = item & 3;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t src = at + r * 256 + hh * 128 + j * 32;
+              x[it][hh][0] = lds16(src);
+              x[it][hh][1] = lds16(src + 16);
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int item = tid + 128 * it;
+            const int r = item >> 2, j = item & 3;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              uint4 x0 = x[it][hh][0], x1 = x[it][hh][1];
+              const int e0 = ch * kKcChunk + hh * 32 + 8 * j;
+              if (e0 >= F) x0 = make_uint4(0, 0, 0, 0);
+              if (e0 + 4 >= F) x1 = make_uint4(0, 0, 0, 0);
+              const uint4 y = a.out_dtype == 2
+                                  ? make_uint4(f16x2(x0.x, x0.y), f16x2(x0.z, x0.w), f16x2(x1.x, x1.y), f16x2(x1.z, x1.w))
+                                  : make_uint4(bf16x2(x0.x, x0.y), bf16x2(x0.z, x0.w), bf16x2(x1.x, x1.y),
+                                               bf16x2(x1.z, x1.w));
+              sts16(at + sw128(r, hh * 4 + j), y);
+            }
+          }
+          bar_arrive(&stg_empty[2 * p + 1]);  // slot 2p + 1 read out (before the barrier); 2p holds A(u)
+          fence_async_smem();
+          if constexpr (kPair)
+            bar_arrive(&a_conv[p]);
+          else
+            bar_arrive(&a_full[p]);
+          continue;
+        }
         for (int hh = 0; hh < 2; ++hh) {
           const int sl = 2 * p + hh;
           bar_wait(&stg_full[sl], ra.ph);
@@ -1554,16 +1619,18 @@ bool encode_a_map_kc(const LinearArgs& a, CUtensorMap* m) {
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// fp32 records: {record element, row} of fp32, box 32 elements (128 B) x 1 row, 128-byte swizzle.
-bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m) {
+// fp32 records: {record element, row} of fp32, box 32 elements (128 B) x 1 row, 128-byte swizzle; or
+// (wide) box 64 elements (256 B) x 1 row, unswizzled: one gather4 per 4 rows of a whole chunk.
+bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m, bool wide) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (encode == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.rec_stride / 4), static_cast<cuuint64_t>(a.shards[0].n_hbm)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.rec_stride)};
-  const cuuint32_t box[2] = {32, 1};
+  const cuuint32_t box[2] = {wide ? 64u : 32u, 1};
   const cuuint32_t estr[2] = {1, 1};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
@@ -1607,7 +1674,11 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   if (!(tf && !strcmp(tf, "0")) && a.in_dtype == 0 && a.F % 4 == 0 && a.world == 1 &&
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
-    a.tma_f32 = encode_a_map_f32_kc(a, &amap) ? 1 : 0;
+  {
+    // PPLOAD_LINEAR_TMA_F32=2: wide unswizzled boxes (half the gather4s; converters 2-way bank conflicts)
+    const int want = tf ? atoi(tf) : 1;
+    a.tma_f32 = encode_a_map_f32_kc(a, &amap, want == 2) ? (want == 2 ? 2 : 1) : 0;
+  }
   // CTA pairs (cta_group::2, M = 256): the default when the A chunks come by TMA (HBM-resident,
   // unsharded stores) -- half the W bytes through each SM's shared memory; interleaved A/B at MAG240M
   // rows 13.0-13.6 vs 16.4-17.9 ms (single CTAs also drop further under the power cap), IGB-large rows

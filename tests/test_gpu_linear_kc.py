@@ -178,11 +178,12 @@ def test_kc_tma_gather4_sixteen_bit(pp, monkeypatch, tma_a, dt, F, chunk):
         run_and_check(pp, L, X, dt, hs, rs, H, F, D, order, B, dt, "f32", k=3)
 
 
-@pytest.mark.parametrize("tma_f32", ["1", "0"])
+@pytest.mark.parametrize("tma_f32", ["1", "0", "2"])
 @pytest.mark.parametrize("F,out_dt,chunk", [(128, oracle.BF16, 1), (192, oracle.F16, 33), (1024, oracle.BF16, 256)])
 def test_kc_tma_gather4_fp32_staging(pp, monkeypatch, tma_f32, F, out_dt, chunk):
     # fp32 records with F % 64 == 0 in HBM: 32-element halves by TMA gather4 into the staging ring,
-    # cast by four converter warps (PPLOAD_LINEAR_TMA_F32=1, default) or the register producers (0)
+    # cast by four converter warps (PPLOAD_LINEAR_TMA_F32=1, default), whole 64-element chunks by
+    # unswizzled 256-byte gather4 boxes (2), or the register producers (0)
     monkeypatch.setenv("PPLOAD_LINEAR_TMA_F32", tma_f32)
     monkeypatch.setenv("PPLOAD_LINEAR", "kc")
     H, N, B, D = 2, 2300, 320, 512
@@ -225,7 +226,7 @@ def test_kc_cta_pair(pp, monkeypatch, pair, H, F, dt, D, B, path):
 
 
 @pytest.mark.parametrize("pair", ["1", "0"])
-@pytest.mark.parametrize("tma_f32", ["1", "0"])
+@pytest.mark.parametrize("tma_f32", ["1", "0", "2"])
 @pytest.mark.parametrize("F", [100, 36, 196])
 def test_kc_fp32_f_not_multiple_of_64(pp, monkeypatch, pair, tma_f32, F):
     # fp32 records with F % 64 != 0 (products F = 100; F % 8 != 0 too): the last K chunk is padded
