@@ -586,9 +586,15 @@ def next_rows_secondary():
     out = {}
     try:
         prop = _script_lines("bench_propagate.py", {}, timeout=240)
-        out["propagation"] = {"ms_per_hop": prop[0]["ms_per_hop"], "frac_hbm": prop[0]["frac_hbm"],
-                              "into_store_ms_per_hop": prop[-1]["ms_per_hop"], "nnz": prop[0]["nnz"],
-                              "note": "bit-identical to the CPU oracle (tests/test_gpu_propagate*.py)"}
+        p0 = prop[0]
+        out["propagation"] = {"ms_per_hop": p0["ms_per_hop"], "frac_hbm": p0["frac_hbm"],
+                              "frac_hbm_basis": "no-reuse bytes (every nonzero reads its neighbour row, column, weight)",
+                              "compulsory_bytes_per_hop": p0.get("compulsory_bytes_per_hop"),
+                              "compulsory_GBs": p0.get("compulsory_GBs"),
+                              "frac_hbm_compulsory": (p0["compulsory_GBs"] / peaks()[0] if "compulsory_GBs" in p0 else None),
+                              "into_store_ms_per_hop": prop[-1]["ms_per_hop"], "nnz": p0["nnz"],
+                              "note": "bit-identical to the CPU oracle (tests/test_gpu_propagate*.py); ncu: 64.7 GB of "
+                                      "DRAM reads per hop (random 400-B rows miss L2), DESIGN.md §12"}
     except Exception as e:
         out["propagation"] = {"error": repr(e)[:300]}
     try:

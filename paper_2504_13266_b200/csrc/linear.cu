@@ -1667,16 +1667,18 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
     a.tma_a = encode_a_map_kc(a, &amap) ? want_tma : 0;
-  // fp32 records: gather4 of 32-element halves into a staging ring, converted by four warps
-  // (PPLOAD_LINEAR_TMA_F32=0 keeps the register-staged producers)
+  // fp32 records: gather4 into a staging ring, converted in place by four warps. Default (2): whole
+  // 64-element chunks as unswizzled 256-byte boxes (half the gather4s; the converters take 2-way bank
+  // conflicts); interleaved A/B at IGB-large rows 15.8-16.9 vs 16.8-18.9 ms per epoch in pairs, 18.8-20.2
+  // vs 20.5-21.3 single (profiles/r2/kc_pair/s2s_ab_wide.jsonl). =1: 128-byte SW128 halves; =0: the
+  // register-staged producers
   const char* tf = getenv("PPLOAD_LINEAR_TMA_F32");
   a.tma_f32 = 0;
   if (!(tf && !strcmp(tf, "0")) && a.in_dtype == 0 && a.F % 4 == 0 && a.world == 1 &&
       a.shards[0].spill == nullptr && a.shards[0].hbm != nullptr && a.shards[0].n_hbm > 0 &&
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
   {
-    // PPLOAD_LINEAR_TMA_F32=2: wide unswizzled boxes (half the gather4s; converters 2-way bank conflicts)
-    const int want = tf ? atoi(tf) : 1;
+    const int want = tf ? atoi(tf) : 2;
     a.tma_f32 = encode_a_map_f32_kc(a, &amap, want == 2) ? (want == 2 ? 2 : 1) : 0;
   }
   // CTA pairs (cta_group::2, M = 256): the default when the A chunks come by TMA (HBM-resident,
