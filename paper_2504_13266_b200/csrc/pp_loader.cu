@@ -607,6 +607,11 @@ pp_status pp_loader_create(const pp_loader_desc* desc, pp_loader** out) {
   L->local_rows = (R - L->rank + L->W - 1) / L->W;
   L->rec_in = static_cast<int64_t>(L->HF) * elem_bytes(L->in_dtype);
   L->rec_stride = (L->rec_in + 15) / 16 * 16;
+  // experiment knob: record pitch rounded up to a power of two >= 16 bytes (e.g. 128: whole L2 lines)
+  if (const char* e = getenv("PPLOAD_REC_ALIGN")) {
+    const int64_t al = atoll(e);
+    if (al >= 16 && (al & (al - 1)) == 0) L->rec_stride = (L->rec_in + al - 1) / al * al;
+  }
   L->rec_out = static_cast<int64_t>(L->HF) * elem_bytes(L->out_dtype);
   L->vector_path = gather_vector_ok(L->HF, L->in_dtype, L->out_dtype, L->rec_stride);
   // the gather kernels divide slot indices by a 2^40 reciprocal: tile (<= 128 rows) x slots per row
