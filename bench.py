@@ -564,7 +564,7 @@ def consumer_fused_linear(pp, torch, cfg, args, D=512, k=8, reps=5):
     return {"value": N / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "hidden": D,
             "achieved_GBs": N * per_node / ms / 1e6, "frac_hbm": N * per_node / ms / 1e6 / peak,
             "tflops": 2.0 * N * H * F * D / ms / 1e9,
-            "note": "fused gather + cast + per-hop linear (tcgen05, TMEM accumulators); "
+            "note": "fused gather + cast + per-hop linear (k_gather_linear_kc: TMA gather4 A chunks, tcgen05 CTA pairs, TMEM accumulators); "
                     "unfused loader + cuBLAS reference: profiles/r1e_bench_fused_linear.jsonl"}
 
 

@@ -319,10 +319,10 @@ pp_status pp_next_batches_ev(pp_loader* L, int32_t n, void* out, int64_t out_str
  *   W: device [H][F][D] row-major in the batch dtype (W_k = W[k] is F x D),
  *      16-B aligned.
  *   D: 256 or 512.  F % 4 == 0 for fp32 records, F % 8 == 0 for 16-bit ones;
- *      any placement (HBM, spilled, sharded W > 1, compact store).  fp32 ->
- *      bf16 HBM stores with F <= 128 and W == 1 take the W-resident kernel,
- *      everything else the K-chunked one (PPLOAD_LINEAR=kc forces it), which
- *      runs as CTA pairs (tcgen05 cta_group::2, clusters of two) when the A
+ *      any placement (HBM, spilled, sharded W > 1, compact store).  Every
+ *      call takes the K-chunked kernel (PPLOAD_LINEAR=res selects the round-1
+ *      W-resident kernel for fp32 -> bf16 HBM stores with F <= 128, W == 1),
+ *      which runs as CTA pairs (tcgen05 cta_group::2, clusters of two) when the A
  *      chunks come by TMA (an unsharded, HBM-resident store; PPLOAD_LINEAR_PAIR
  *      = 0 / 1 forces single CTAs / pairs).  Results are identical either way
  *      up to fp32 accumulation order.

@@ -123,6 +123,8 @@ struct LinearArgs {
   ShardView shards[kMaxWorld];
   int32_t tma_a = 0;                    // set by launch_gather_linear_kc: A chunks by TMA tile::gather4
   int32_t tma_f32 = 0;                  // set by launch_gather_linear_kc: fp32 records by gather4 into staging
+  int32_t hop_rows = 0;                 // set by launch_gather_linear_kc: the fp32 A map is [rows x H][F] (hop k of
+                                        // node v = map row v H + k; K padding zero-filled out of bounds)
   int32_t pair = 0;                     // set by launch_gather_linear_kc: CTA pairs (cta_group::2, M = 256)
   int32_t units = 0;                    // set by launch_gather_linear_kc: (tile, hop) units over the whole grid
 };

@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           v = a.order[pos + r0 + j];
           if (a.node_set != nullptr) v = a.node_set[v];
         }
-        s_rows[j] = static_cast<int32_t>(v);
+        s_rows[j] = static_cast<int32_t>(a.hop_rows ? v * H + k : v);
       }
       __syncwarp();
       for (int ch = 0; ch < nch; ++ch) {
@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
               asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[2 * p])),
                            "r"(2 * kKcABytes)
                            : "memory");
-            const int col = k * F + ch * kKcChunk;
+            const int col = (a.hop_rows ? 0 : k * F) + ch * kKcChunk;
             uint8_t* dst = a_s + 2 * p * kKcABytes;
             for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
               asm volatile(
@@ -1103,7 +1103,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[sl])),
                              "r"(kKcABytes)
                              : "memory");
-              const int col = k * F + ch * kKcChunk + hh * 32;
+              const int col = (a.hop_rows ? 0 : k * F) + ch * kKcChunk + hh * 32;
               uint8_t* dst = a_s + sl * kKcABytes;
               for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
                 asm volatile(
@@ -1621,11 +1621,15 @@ bool encode_a_map_kc(const LinearArgs& a, CUtensorMap* m) {
 }
 // fp32 records: {record element, row} of fp32, box 32 elements (128 B) x 1 row, 128-byte swizzle; or
 // (wide) box 64 elements (256 B) x 1 row, unswizzled: one gather4 per 4 rows of a whole chunk.
-bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m, bool wide) {
+// hop_rows: the map is {hop element, (node, hop) row} with row pitch F * 4 (records unpadded: rec_stride
+// == H F 4), so a chunk past F reads nothing -- the K padding is the out-of-bounds zero fill instead of
+// the next hop's bytes (products' F = 100: 400 instead of 512 bytes per row and hop).
+bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m, bool wide, bool hop_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (encode == nullptr) return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.rec_stride / 4), static_cast<cuuint64_t>(a.shards[0].n_hbm)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.rec_stride)};
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hop_rows ? a.F : a.rec_stride / 4),
+                              static_cast<cuuint64_t>(a.shards[0].n_hbm * (hop_rows ? a.H : 1))};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(hop_rows ? a.F * 4 : a.rec_stride)};
   const cuuint32_t box[2] = {wide ? 64u : 32u, 1};
   const cuuint32_t estr[2] = {1, 1};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
@@ -1679,7 +1683,11 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
       a.shards[0].n_hbm < (int64_t(1) << 31) && a.rec_stride % 16 == 0)
   {
     const int want = tf ? atoi(tf) : 2;
-    a.tma_f32 = encode_a_map_f32_kc(a, &amap, want == 2) ? (want == 2 ? 2 : 1) : 0;
+    // (node, hop) rows when the records are unpadded and F % 64 != 0 (experiment bit 524288: off)
+    const bool hop_rows = a.F % kKcChunk != 0 && a.rec_stride == static_cast<int64_t>(a.H) * a.F * 4 &&
+                          a.shards[0].n_hbm * a.H < (int64_t(1) << 31) && (a.debug & 524288) == 0;
+    a.tma_f32 = encode_a_map_f32_kc(a, &amap, want == 2, hop_rows) ? (want == 2 ? 2 : 1) : 0;
+    a.hop_rows = a.tma_f32 && hop_rows ? 1 : 0;
   }
   // CTA pairs (cta_group::2, M = 256): the default when the A chunks come by TMA (HBM-resident,
   // unsharded stores) -- half the W bytes through each SM's shared memory; interleaved A/B at MAG240M

@@ -1493,11 +1493,13 @@ pp_status pp_next_batches_linear(pp_loader* L, int32_t n, const void* W, int32_t
   if (!rows || n < 1 || !W || !Z) return fail(PP_ERR_INVALID, "NULL argument or n < 1");
   if (L->files) return fail(PP_ERR_INVALID, "fused linear needs an in-memory store (not the storage tier)");
   if (L->out_dtype == PP_F32) return fail(PP_ERR_INVALID, "fused linear needs a 16-bit batch dtype (bf16 / f16)");
-  // the F <= 128 kernel (W_k resident in shared memory) for fp32 -> bf16 unsharded HBM stores; the
-  // K-chunked kernel for every other shape, dtype and placement
+  // the K-chunked kernel for every shape, dtype and placement; the round-1 kernel with W_k resident in
+  // shared memory (fp32 -> bf16 unsharded HBM stores, F <= 128) only on request (PPLOAD_LINEAR=res):
+  // at the products shape the K-chunked CTA pairs measured 2.99-3.00 vs 3.13 ms per epoch (interleaved
+  // A/B medians, profiles/r2/kc_pair/s3a_ab_products.jsonl, s3c_ab_products.jsonl)
   const char* kc_env = getenv("PPLOAD_LINEAR");
   const bool resident = L->in_dtype == PP_F32 && L->out_dtype == PP_BF16 && L->n_spill == 0 && L->W == 1 &&
-                        linear_supported(L->H, L->F, D, L->num_sms) && !(kc_env && !strcmp(kc_env, "kc"));
+                        linear_supported(L->H, L->F, D, L->num_sms) && kc_env && !strcmp(kc_env, "res");
   if (!resident && !linear_kc_supported(L->H, L->F, D, L->num_sms, L->in_dtype, L->out_dtype))
     return fail(PP_ERR_INVALID, "fused linear supports F %% 4 == 0 (fp32 records) or F %% 8 == 0 (16-bit records) and D in {256, 512} "
                 "(F=%d, D=%d)", L->F, D);

@@ -72,9 +72,9 @@ def timeit(fn, reps=5):
 
 
 # variants timed in interleaved rounds (box-to-box and power-state drift hits all alike); the
-# fused kernel is the W-resident one by default, PPLOAD_LINEAR=kc forces the K-chunked one
+# fused kernel is the K-chunked one by default (round 2), PPLOAD_LINEAR=res selects the W-resident one
 VARIANTS = [("fused_tcgen05", fused_epoch, "", H * F * 4 + H * D * 2 + 4),
-            ("fused_tcgen05_kc", fused_epoch, "kc", H * F * 4 + H * D * 2 + 4),
+            ("fused_tcgen05_resident", fused_epoch, "res", H * F * 4 + H * D * 2 + 4),
             ("unfused_gather_then_cublas", unfused_epoch, "", H * F * 4 + H * F * 2 + 4 + H * F * 2 + H * D * 2)]
 times = {v[0]: [] for v in VARIANTS}
 for rnd in range(int(os.environ.get("LIN_ROUNDS", "3"))):

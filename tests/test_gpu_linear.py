@@ -16,6 +16,13 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+@pytest.fixture(autouse=True, params=["res", "auto"])
+def kernel(request, monkeypatch):
+    # every case on the W-resident kernel (PPLOAD_LINEAR=res) and on the default K-chunked one
+    monkeypatch.setenv("PPLOAD_LINEAR", request.param)
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def pp():
     import __graft_entry__ as ge

@@ -225,17 +225,24 @@ def test_kc_cta_pair(pp, monkeypatch, pair, H, F, dt, D, B, path):
         run_and_check(pp, L, bits, dt, hs, rs, H, F, D, order, B, out_dt, zdt, k=3)
 
 
+@pytest.mark.parametrize("layout", ["hop_rows", "records", "padded"])
 @pytest.mark.parametrize("pair", ["1", "0"])
 @pytest.mark.parametrize("tma_f32", ["1", "0", "2"])
 @pytest.mark.parametrize("F", [100, 36, 196])
-def test_kc_fp32_f_not_multiple_of_64(pp, monkeypatch, pair, tma_f32, F):
+def test_kc_fp32_f_not_multiple_of_64(pp, monkeypatch, pair, tma_f32, F, layout):
     # fp32 records with F % 64 != 0 (products F = 100; F % 8 != 0 too): the last K chunk is padded
     # with zeros -- the fp32 gather4 reads 32-element halves that run into the next hop, which the
     # converters must zero (Inf planted at the start of hop 1 would otherwise poison hop 0's sums:
-    # 0 * Inf = NaN); F <= 128 keeps W_k resident in the W stages (<= 256 for pairs)
+    # 0 * Inf = NaN); F <= 128 keeps W_k resident in the W stages (<= 256 for pairs).
+    # layout: the TMA map of (node, hop) rows whose K padding is the out-of-bounds zero fill (default),
+    # the map of whole records (experiment bit 524288), or records padded to 128 B (PPLOAD_REC_ALIGN)
     monkeypatch.setenv("PPLOAD_LINEAR", "kc")
     monkeypatch.setenv("PPLOAD_LINEAR_PAIR", pair)
     monkeypatch.setenv("PPLOAD_LINEAR_TMA_F32", tma_f32)
+    if layout == "records":
+        monkeypatch.setenv("PPLOAD_DEBUG_LINEAR", "524288")
+    elif layout == "padded":
+        monkeypatch.setenv("PPLOAD_REC_ALIGN", "128")
     H, N, B, D = 3, 3001, 640, 512
     X, hs, rs = hop_tensor(120 + F, H, N, F)
     trap = np.random.default_rng(121).choice(N, 64, replace=False)
