@@ -1492,6 +1492,16 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         if (c_lo >= c_hi) continue;
         bar_wait(&t_full[h], i & 1);
         tc_fence_after();
+        if (a.debug & 2097152) {  // experiment: no accumulator drain at all (no TMEM loads, no Z)
+          tc_fence_before();
+          if constexpr (kPair) {
+            __syncwarp();
+            if (lane == 0) bar_arrive_remote_tmem(leader_addr(&t_empty[h]));
+          } else {
+            arrive_leader(&t_empty[h]);
+          }
+          continue;
+        }
         const uint32_t trow = tmem + (static_cast<uint32_t>(e * 32) << 16) + h * kUmmaN;
         uint32_t v[64];
         auto ld_slice = [&](int c0) {
