@@ -1053,22 +1053,54 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     __shared__ int32_t s_rows[kTileM];
     const uint64_t amap_addr = reinterpret_cast<uint64_t>(&amap);
     Ring ra(na);
-    for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride)) {
+    // L2 prefetch (a.l2_prefetch, PPLOAD_LINEAR_PREFETCH=1; off by default): after issuing unit u, every
+    // lane pulls its row of the next unit into L2 (one cp.async.bulk.prefetch of the hop's F * s_in
+    // bytes). Measured: products 1-2 % faster, MAG240M / IGB-large rows 3 % / 27 % slower (s3k_ab.jsonl)
+    const int jrow = warp * (kTileM / gw) + lane;
+    const bool jown = lane < kTileM / gw;
+    for (int64_t u = next_unit(ufirst); u < nunits;) {
+      const int64_t un = next_unit(u + ustride);
       const int64_t t = set_unit(u);
       int64_t step, pos;
       int r0;
       const int rows = tile_rows_cta(t, step, r0, pos);
       __syncwarp();
-      for (int j = warp * (kTileM / gw) + lane; j < (warp + 1) * (kTileM / gw); j += 32) {
+      if (jown) {
         int64_t v = 0;  // rows past the batch gather record 0; the epilogue never stores them
-        if (j < rows) {
-          v = a.order[pos + r0 + j];
+        if (jrow < rows) {
+          v = a.order[pos + r0 + jrow];
           if (a.node_set != nullptr) v = a.node_set[v];
         }
-        s_rows[j] = static_cast<int32_t>(a.hop_rows ? v * H + k : v);
+        s_rows[jrow] = static_cast<int32_t>(a.hop_rows ? v * H + k : v);
       }
       __syncwarp();
       for (int ch = 0; ch < nch; ++ch) {
+        if (a.tma_f32 == 3) {  // fp32 records, 64 < F <= 128, pairs: one 512-byte box per (node, hop) row
+          if (lane == 0) {     // covers both chunks: 32 gather4 into slots 2p .. 2p + 3 (p even) at chunk 0
+            const int p = ra.s;
+            const uint32_t ph = ra.ph;
+            ra.next();
+            if (ch == 0) {
+              bar_wait(&a_empty[p], ph ^ 1u);
+              bar_wait(&stg_empty[2 * p + 1], ph ^ 1u);
+              bar_wait(&a_empty[p + 1], ph ^ 1u);
+              bar_wait(&stg_empty[2 * p + 3], ph ^ 1u);
+              if (warp == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&stg_full[2 * p])),
+                             "r"(4 * kKcABytes)
+                             : "memory");
+              uint8_t* dst = a_s + 2 * p * kKcABytes;
+              for (int g = warp * (32 / gw); g < (warp + 1) * (32 / gw); ++g)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 2048)),
+                    "l"(amap_addr), "r"(0), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
+                    "r"(s_rows[4 * g + 3]), "r"(smem_addr(&stg_full[2 * p]))
+                    : "memory");
+            }
+          }
+          continue;
+        }
         if (a.tma_f32 == 2) {  // fp32 records, wide boxes: the whole 64-element chunk (4 rows x 256 B per
           if (lane == 0) {     // gather4, unswizzled) into slots 2p, 2p + 1 as 128 rows of 256 B
             const int p = ra.s;
@@ -1129,6 +1161,19 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                                s_rows[4 * g + 2], s_rows[4 * g + 3], fb);
         }
       }
+      if (a.l2_prefetch && jown && un < nunits) {
+        int64_t stn, psn;
+        int r0n;
+        const int rowsn = tile_rows_cta(unit_tile(un), stn, r0n, psn);
+        if (jrow < rowsn) {
+          int64_t v = a.order[psn + r0n + jrow];
+          if (a.node_set != nullptr) v = a.node_set[v];
+          const int kn = a.units ? static_cast<int>(un % H) : k;
+          const uint8_t* pr = a.shards[0].hbm + v * a.rec_stride + static_cast<int64_t>(kn) * F * s_in;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(F * s_in) : "memory");
+        }
+      }
+      u = un;
     }
     __syncwarp();
   } else if (a.tma_f32 && warp < kProducerWarps) {
@@ -1144,6 +1189,63 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int ch = 0; ch < nch; ++ch, ra.next()) {
         const int p = ra.s;
         const uint32_t at = a_base + 2 * p * kKcABytes;
+        if (a.tma_f32 == 3) {
+          // one tile's rows staged at chunk 0 (p even): staged row r = 512 B (128 fp32, zero past F) at
+          // 2p * 16 KB + 512 r, i.e. rows 32i..32i+31 in slot 2p + i. A chunk 0 goes to slot 2p, chunk 1
+          // to slot 2p + 2 (where the MMA reads ring positions p and p + 1), so only staged rows 0-31 and
+          // 64-95 are overwritten: those are read into registers first, the four converter warps meet at
+          // a named barrier, then they are written; rows 32-63 and 96-127 (slots 2p + 1, 2p + 3, never
+          // written) are converted straight from shared memory
+          if (ch != 0) continue;
+          bar_wait(&stg_full[2 * p], ra.ph);
+          const uint32_t a1 = at + 2 * kKcABytes;
+          auto cvt_store = [&](int r, int j8, uint4 x0, uint4 x1) {
+            const int e0 = 8 * j8;
+            if (e0 >= F) x0 = make_uint4(0, 0, 0, 0);
+            if (e0 + 4 >= F) x1 = make_uint4(0, 0, 0, 0);
+            const uint4 y = a.out_dtype == 2
+                                ? make_uint4(f16x2(x0.x, x0.y), f16x2(x0.z, x0.w), f16x2(x1.x, x1.y), f16x2(x1.z, x1.w))
+                                : make_uint4(bf16x2(x0.x, x0.y), bf16x2(x0.z, x0.w), bf16x2(x1.x, x1.y),
+                                             bf16x2(x1.z, x1.w));
+            sts16(((j8 >> 3) ? a1 : at) + sw128(r, j8 & 7), y);
+          };
+          uint4 x[8][2];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int item = tid + 128 * it;  // (row index 0..63, 32-byte group j8 of 16)
+            const int ri = item >> 4, j8 = item & 15;
+            const int r = ri < 32 ? ri : ri + 32;
+            const uint32_t src = at + r * 512 + j8 * 32;
+            x[it][0] = lds16(src);
+            x[it][1] = lds16(src + 16);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int item = tid + 128 * it;
+            const int ri = item >> 4, j8 = item & 15;
+            cvt_store(ri < 32 ? ri : ri + 32, j8, x[it][0], x[it][1]);
+          }
+#pragma unroll 2
+          for (int it = 0; it < 8; ++it) {
+            const int item = tid + 128 * it;
+            const int ri = item >> 4, j8 = item & 15;
+            const int r = ri < 32 ? ri + 32 : ri + 64;
+            const uint32_t src = at + r * 512 + j8 * 32;
+            cvt_store(r, j8, lds16(src), lds16(src + 16));
+          }
+          bar_arrive(&stg_empty[2 * p + 1]);
+          bar_arrive(&stg_empty[2 * p + 3]);
+          fence_async_smem();
+          if constexpr (kPair) {
+            bar_arrive(&a_conv[p]);
+            bar_arrive(&a_conv[p + 1]);
+          } else {
+            bar_arrive(&a_full[p]);
+            bar_arrive(&a_full[p + 1]);
+          }
+          continue;
+        }
         if (a.tma_f32 == 2) {
           // wide boxes: staging row r = 256 B (64 fp32) at 2p * 16 KB + 256 r; the A chunk (rows of 128 B,
           // SW128) overwrites staging rows 0-63, which other warps' threads read -- so every thread reads
@@ -1634,14 +1736,15 @@ bool encode_a_map_kc(const LinearArgs& a, CUtensorMap* m) {
 // hop_rows: the map is {hop element, (node, hop) row} with row pitch F * 4 (records unpadded: rec_stride
 // == H F 4), so a chunk past F reads nothing -- the K padding is the out-of-bounds zero fill instead of
 // the next hop's bytes (products' F = 100: 400 instead of 512 bytes per row and hop).
-bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m, bool wide, bool hop_rows) {
+bool encode_a_map_f32_kc(const LinearArgs& a, CUtensorMap* m, bool wide, bool hop_rows, bool tile = false) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (encode == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hop_rows ? a.F : a.rec_stride / 4),
                               static_cast<cuuint64_t>(a.shards[0].n_hbm * (hop_rows ? a.H : 1))};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(hop_rows ? a.F * 4 : a.rec_stride)};
-  const cuuint32_t box[2] = {wide ? 64u : 32u, 1};
+  const cuuint32_t box[2] = {tile ? 128u : wide ? 64u : 32u, 1};
   const cuuint32_t estr[2] = {1, 1};
+  wide = wide || tile;
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(a.shards[0].hbm), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                 wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1709,6 +1812,20 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   if (a.debug & 8192) pair = !pair;
   pair = pair && (a.num_sms / 2) >= a.H && (a.debug & 2048) == 0;
   a.pair = pair ? 1 : 0;
+  // experiment bit 4194304 (fp32 records with 64 < F <= 128 in pairs, A ring of 4 chunk positions): one
+  // 512-byte gather4 box per (node, hop) row stages both chunks of a tile at once -- half the gather4 row
+  // requests of the 256-byte boxes. Measured no faster at the products shape (A side alone 1.65 vs
+  // 1.56 ms per epoch, whole kernel equal; profiles/r2/kc_products/s3j_ab.jsonl, s3k_ab.jsonl), so off
+  if (pair && a.tma_f32 == 2 && a.F > kKcChunk && a.F <= 2 * kKcChunk &&
+      a.rec_stride == static_cast<int64_t>(a.H) * a.F * 4 && a.shards[0].n_hbm * a.H < (int64_t(1) << 31) &&
+      (a.debug & 4194304) != 0 && (a.debug & 524288) == 0) {
+    alignas(64) CUtensorMap tmap{};
+    if (encode_a_map_f32_kc(a, &tmap, true, true, true)) {
+      amap = tmap;
+      a.tma_f32 = 3;
+      a.hop_rows = 1;
+    }
+  }
   // (tile, hop) work units over the whole grid when W_k is streamed per tile (F > 128) and the A
   // chunks come by TMA (the register producers keep hop-pinned CTAs); experiment bit 262144: off
   const bool w_resident = (a.F + kKcChunk - 1) / kKcChunk <= 2;

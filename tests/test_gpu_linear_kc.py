@@ -292,3 +292,24 @@ def test_kc_cta_pair_sharded_loopback(pp, monkeypatch, W):
     finally:
         for L in Ls:
             L.close()
+
+
+@pytest.mark.parametrize("F,chunk", [(100, 1), (68, 1), (128, 9), (124, 1)])
+@pytest.mark.parametrize("prefetch", ["0", "1"])
+def test_kc_fp32_whole_tile_boxes_and_prefetch(pp, monkeypatch, F, chunk, prefetch):
+    # experiment bit 4194304: 64 < F <= 128 fp32 records in pairs, one 512-byte gather4 box per (node, hop)
+    # row stages both chunks of a tile, converted in place into slots 2p and 2p + 2; PPLOAD_LINEAR_PREFETCH=1:
+    # the TMA producers pull the next unit's rows into L2. Inf at the next hop's start must not leak.
+    monkeypatch.setenv("PPLOAD_LINEAR", "kc")
+    monkeypatch.setenv("PPLOAD_LINEAR_PAIR", "1")
+    monkeypatch.setenv("PPLOAD_DEBUG_LINEAR", "4194304")
+    monkeypatch.setenv("PPLOAD_LINEAR_PREFETCH", prefetch)
+    H, N, B, D = 3, 4099, 896, 512
+    X, hs, rs = hop_tensor(140 + F, H, N, F)
+    trap = np.random.default_rng(141).choice(N, 64, replace=False)
+    X[1, trap, :4] = np.inf
+    with pp.Loader(data=X, num_nodes=N, num_hops=H, feat_dim=F, hop_stride=hs, row_stride=rs, dtype=pp.PP_F32,
+                   batch_size=B, out_dtype=pp.PP_BF16) as L:
+        L.epoch_permute(16, chunk)
+        order = oracle.epoch_order(16, N, chunk)
+        run_and_check(pp, L, X.view(np.uint32), oracle.F32, hs, rs, H, F, D, order, B, oracle.BF16, "bf16", k=3)
