@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
             const int p = ra.s;
             const uint32_t ph = ra.ph;
             ra.next();
-            if (ch == 0) {
+            if ((ch & 1) == 0) {  // chunks ch, ch + 1 (nch even)
               bar_wait(&a_empty[p], ph ^ 1u);
               bar_wait(&stg_empty[2 * p + 1], ph ^ 1u);
               bar_wait(&a_empty[p + 1], ph ^ 1u);
@@ -1094,8 +1094,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                 asm volatile(
                     "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
                     " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(dst + g * 2048)),
-                    "l"(amap_addr), "r"(0), "r"(s_rows[4 * g]), "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]),
-                    "r"(s_rows[4 * g + 3]), "r"(smem_addr(&stg_full[2 * p]))
+                    "l"(amap_addr), "r"((a.hop_rows ? 0 : k * F) + ch * kKcChunk), "r"(s_rows[4 * g]),
+                    "r"(s_rows[4 * g + 1]), "r"(s_rows[4 * g + 2]), "r"(s_rows[4 * g + 3]), "r"(smem_addr(&stg_full[2 * p]))
                     : "memory");
             }
           }
@@ -1196,11 +1196,11 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           // 64-95 are overwritten: those are read into registers first, the four converter warps meet at
           // a named barrier, then they are written; rows 32-63 and 96-127 (slots 2p + 1, 2p + 3, never
           // written) are converted straight from shared memory
-          if (ch != 0) continue;
+          if (ch & 1) continue;
           bar_wait(&stg_full[2 * p], ra.ph);
           const uint32_t a1 = at + 2 * kKcABytes;
           auto cvt_store = [&](int r, int j8, uint4 x0, uint4 x1) {
-            const int e0 = 8 * j8;
+            const int e0 = ch * kKcChunk + 8 * j8;
             if (e0 >= F) x0 = make_uint4(0, 0, 0, 0);
             if (e0 + 4 >= F) x1 = make_uint4(0, 0, 0, 0);
             const uint4 y = a.out_dtype == 2
@@ -1799,7 +1799,7 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
     // (node, hop) rows when the records are unpadded and F % 64 != 0 (experiment bit 524288: off)
     const bool hop_rows = a.F % kKcChunk != 0 && a.rec_stride == static_cast<int64_t>(a.H) * a.F * 4 &&
                           a.shards[0].n_hbm * a.H < (int64_t(1) << 31) && (a.debug & 524288) == 0;
-    a.tma_f32 = encode_a_map_f32_kc(a, &amap, want == 2, hop_rows) ? (want == 2 ? 2 : 1) : 0;
+    a.tma_f32 = encode_a_map_f32_kc(a, &amap, want >= 2, hop_rows) ? (want >= 2 ? 2 : 1) : 0;
     a.hop_rows = a.tma_f32 && hop_rows ? 1 : 0;
   }
   // CTA pairs (cta_group::2, M = 256): the default when the A chunks come by TMA (HBM-resident,
@@ -1816,14 +1816,19 @@ cudaError_t launch_gather_linear_kc(const LinearArgs& a_in, bool pdl, cudaStream
   // 512-byte gather4 box per (node, hop) row stages both chunks of a tile at once -- half the gather4 row
   // requests of the 256-byte boxes. Measured no faster at the products shape (A side alone 1.65 vs
   // 1.56 ms per epoch, whole kernel equal; profiles/r2/kc_products/s3j_ab.jsonl, s3k_ab.jsonl), so off
-  if (pair && a.tma_f32 == 2 && a.F > kKcChunk && a.F <= 2 * kKcChunk &&
-      a.rec_stride == static_cast<int64_t>(a.H) * a.F * 4 && a.shards[0].n_hbm * a.H < (int64_t(1) << 31) &&
-      (a.debug & 4194304) != 0 && (a.debug & 524288) == 0) {
+  // Generalised to any even number of chunks (F > 64): chunk pairs (2c, 2c + 1) as one 512-byte box per row
+  // (PPLOAD_LINEAR_TMA_F32=3 or the bit; the (node, hop) row map when F % 64 != 0, else the record map)
+  const int nch_ = (a.F + kKcChunk - 1) / kKcChunk;
+  const bool want3 = (a.debug & 4194304) != 0 || (tf && atoi(tf) == 3);
+  if (pair && a.tma_f32 == 2 && a.F > kKcChunk && nch_ % 2 == 0 && want3) {
+    const bool hr = a.F % kKcChunk != 0;  // the record map reads whole 128-element boxes inside the hop
     alignas(64) CUtensorMap tmap{};
-    if (encode_a_map_f32_kc(a, &tmap, true, true, true)) {
+    if ((!hr || (a.rec_stride == static_cast<int64_t>(a.H) * a.F * 4 &&
+                 a.shards[0].n_hbm * a.H < (int64_t(1) << 31) && (a.debug & 524288) == 0)) &&
+        encode_a_map_f32_kc(a, &tmap, true, hr, true)) {
       amap = tmap;
       a.tma_f32 = 3;
-      a.hop_rows = 1;
+      a.hop_rows = hr ? 1 : 0;
     }
   }
   // (tile, hop) work units over the whole grid when W_k is streamed per tile (F > 128) and the A

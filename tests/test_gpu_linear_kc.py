@@ -294,11 +294,12 @@ def test_kc_cta_pair_sharded_loopback(pp, monkeypatch, W):
             L.close()
 
 
-@pytest.mark.parametrize("F,chunk", [(100, 1), (68, 1), (128, 9), (124, 1)])
+@pytest.mark.parametrize("F,chunk", [(100, 1), (68, 1), (128, 9), (124, 1), (1024, 1), (196, 5), (256, 1)])
 @pytest.mark.parametrize("prefetch", ["0", "1"])
 def test_kc_fp32_whole_tile_boxes_and_prefetch(pp, monkeypatch, F, chunk, prefetch):
-    # experiment bit 4194304: 64 < F <= 128 fp32 records in pairs, one 512-byte gather4 box per (node, hop)
-    # row stages both chunks of a tile, converted in place into slots 2p and 2p + 2; PPLOAD_LINEAR_PREFETCH=1:
+    # experiment bit 4194304: fp32 records with an even number of 64-element chunks in pairs, one 512-byte
+    # gather4 box per row stages chunks 2c, 2c + 1 of a tile, converted in place into slots 2p and 2p + 2
+    # (F % 64 != 0: the (node, hop) row map, zero fill past F); PPLOAD_LINEAR_PREFETCH=1:
     # the TMA producers pull the next unit's rows into L2. Inf at the next hop's start must not leak.
     monkeypatch.setenv("PPLOAD_LINEAR", "kc")
     monkeypatch.setenv("PPLOAD_LINEAR_PAIR", "1")
