@@ -1562,15 +1562,22 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     __syncwarp();
   } else if (kPair && a.tma_f32 && warp == kKcRelayWarp) {
     // ---------------- pair mode, fp32 records: one lane forwards "chunk u converted" (the 128 converter
-    // threads' local arrivals, acquired here) to the leader's a_full with one cluster-scope release per
-    // chunk -- a per-warp release.cluster arrival on the converters' own path (MEMBAR.ALL.GPU each) made
-    // the pair 1.3x slower than single CTAs at IGB-large rows (r2 second session)
+    // threads' local arrivals, acquired here; their generic stores were made visible to the async proxy
+    // by fence.proxy.async before those arrivals) to the leader's a_full with a default-semantics remote
+    // arrival, as CUTLASS's ClusterBarrier::arrive(cta_id) does for UMMA operands written by threads.
+    // A .release.cluster arrival compiles to MEMBAR.ALL.GPU on every chunk's handoff chain: interleaved
+    // A/B (r2 third session, profiles/r2/kc_products/s3y_ab.jsonl) IGB-large rows 15.0-15.3 vs 15.9-17.3 ms
+    // per epoch (A side alone 10.4-11.3 vs 16.2-16.6), products 2.88-2.92 vs 2.94-3.05; experiment bit
+    // 67108864 restores the release.cluster arrival
     if (lane == 0) {
       Ring ra(na);
       for (int64_t u = next_unit(ufirst); u < nunits; u = next_unit(u + ustride))
         for (int ch = 0; ch < nch; ++ch, ra.next()) {
           bar_wait(&a_conv[ra.s], ra.ph);
-          bar_arrive_remote(leader_addr(&a_full[ra.s]));
+          if (a.debug & 67108864)
+            bar_arrive_remote(leader_addr(&a_full[ra.s]));
+          else
+            bar_arrive_remote_tmem(leader_addr(&a_full[ra.s]));
         }
     }
     __syncwarp();
