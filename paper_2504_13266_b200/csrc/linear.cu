@@ -1626,19 +1626,38 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           ++slice;
           uint8_t* my = sb + lane * 128;
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (a.z_elem == 2) {
+          const bool more = c0 + cols_per_slice < c_hi;
+          if (a.z_elem == 2 && !(a.debug & 134217728)) {
+            // bf16 Z: the next slice's first 32 columns load into v[0..31] as soon as this slice's first
+            // half is staged, so the TMEM load latency overlaps the second half's conversion and stores
+            // (experiment bit 134217728: both loads after all eight stores)
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 4; ++j)
               *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
                   make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
                              bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
-          } else {
+            if (more) PPL_TMEM_LD32(trow + c0 + cols_per_slice, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 4; j < 8; ++j)
               *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
-                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                  make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                             bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            if (more) PPL_TMEM_LD32(trow + c0 + cols_per_slice + 32, (v + 32));
+          } else {
+            if (a.z_elem == 2) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(bf16x2(v[8 * j], v[8 * j + 1]), bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               bf16x2(v[8 * j + 4], v[8 * j + 5]), bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            if (more) ld_slice(c0 + cols_per_slice);
           }
-          if (c0 + cols_per_slice < c_hi) ld_slice(c0 + cols_per_slice);
           __syncwarp();
           if (a.debug & 2) continue;  // experiment: no Z stores
           if (tma_rows) {
